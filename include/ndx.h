@@ -1,0 +1,148 @@
+/*
+ * ndx.h -- C ABI of the B200 device layer (libndx.so).
+ *
+ * This is the thin C layer the C++ host runtime (include/ndactor/*.hpp,
+ * libndactor.so) calls, and the surface any other FFI (ctypes, cgo, JNI)
+ * binds.  It replaces the reference's CPU-simulated OpenCL device
+ * (p/core/include/ndactor/device.hpp:26-86, p/core/src/device.cpp) and its
+ * host-lambda "kernels" (p/core/include/ndactor/kernel.hpp:181-193) with CUDA
+ * streams, events, stream-ordered allocations and sm_100a kernels.
+ *
+ * Conventions
+ *   - Every function returns 0 on success, otherwise a cudaError_t value or
+ *     one of the NDX_E_* codes below; ndx_error_string() names it.  Nothing
+ *     throws across this boundary.
+ *   - Pointers named d_* are device pointers, h_* host pointers.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - Launches are asynchronous and thread-safe per stream.
+ *
+ * p/ = /root/reference/proj/ in the citations below.
+ */
+#ifndef NDX_H
+#define NDX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NDX_E_INVALID 10001    /* bad argument (null pointer, size)       */
+#define NDX_E_TOO_LARGE 10002  /* input exceeds the u32 index format      */
+#define NDX_E_NO_DEVICE 10003  /* no CUDA device / extension unusable     */
+
+const char* ndx_error_string(int code);
+/* Version of the ABI; bumped on any signature change. */
+int ndx_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Device, streams, events, memory.
+ * Replace Device (device.hpp:26-86), Event (event.hpp:22-57) and the
+ * Buffer storage (buffer.hpp:27-40) of the simulated backend.
+ * ------------------------------------------------------------------------- */
+int ndx_device_count(int* count);
+int ndx_device_open(int ordinal);           /* cudaSetDevice + mempool setup */
+int ndx_device_sm_count(int ordinal, int* sms);
+int ndx_device_synchronize(void);
+
+int ndx_stream_create(void** stream);       /* non-blocking stream */
+int ndx_stream_destroy(void* stream);
+int ndx_stream_synchronize(void* stream);
+/* 0 = all work done, 1 = still running, else an error */
+int ndx_stream_query(void* stream);
+
+int ndx_event_create(void** event, int timing);
+int ndx_event_destroy(void* event);
+int ndx_event_record(void* event, void* stream);
+int ndx_event_query(void* event);           /* 0 = complete, 1 = pending */
+int ndx_event_synchronize(void* event);
+int ndx_stream_wait_event(void* stream, void* event);
+int ndx_event_elapsed_ms(void* start, void* stop, float* ms);
+
+/* Stream-ordered allocation from the device's memory pool
+ * (create_buffer / free_buffer, device.cpp:228-249). */
+int ndx_malloc_async(void** d_ptr, size_t bytes, void* stream);
+int ndx_free_async(void* d_ptr, void* stream);
+int ndx_memset_async(void* d_ptr, int value, size_t bytes, void* stream);
+int ndx_host_alloc(void** h_ptr, size_t bytes);   /* pinned */
+int ndx_host_free(void* h_ptr);
+/* enqueue_write_bytes / enqueue_read_bytes (device.cpp:253-283) */
+int ndx_memcpy_h2d_async(void* d_dst, const void* h_src, size_t bytes, void* stream);
+int ndx_memcpy_d2h_async(void* h_dst, const void* d_src, size_t bytes, void* stream);
+int ndx_memcpy_d2d_async(void* d_dst, const void* d_src, size_t bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * WAH index build: the four device stages.
+ * Replaces wah::build_index (p/core/src/wah_builder.cpp:38-307).
+ *
+ *   S1 plan   keys[n]            -> ctl (histograms, key range, sort plan)
+ *   S2 sort   keys[n] + ctl      -> pairs[n]  (stable by key; row ids made on the fly)
+ *   S3 emit   pairs[n] + ctl     -> words[<=2n], vstart[<=n], values[<=n], ctl.{words,distinct}
+ *   S4 table  values, vstart     -> entries[3*D] (value, offset, length)
+ *
+ * `ctl` is a device block of ndx_wah_ctl_bytes() bytes; its first 24 bytes
+ * are an ndx_wah_counts the host may read back after S3.
+ * Scratch buffers must be zero-filled once after allocation.  `epoch` is a
+ * caller-managed counter: each build must use a value not used with the same
+ * scratch since it was last zeroed; a build consumes epoch .. epoch+7.
+ * n must be below 2^31 (the word offsets of the index format are u32).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t words;     /* W: compressed words in the index         */
+  uint64_t distinct;  /* D: distinct values (index entries)        */
+  uint32_t min_key;
+  uint32_t max_key;
+} ndx_wah_counts;
+
+size_t ndx_wah_ctl_bytes(void);
+size_t ndx_wah_sort_scratch_bytes(uint64_t n);
+size_t ndx_wah_emit_scratch_bytes(uint64_t n);
+
+int ndx_wah_plan(const uint32_t* d_keys, uint64_t n, void* d_ctl, void* stream);
+int ndx_wah_sort(const uint32_t* d_keys, uint64_t n, uint32_t row_base,
+                 void* d_ctl, uint64_t* d_pairs, void* d_scratch,
+                 uint32_t epoch, void* stream);
+int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl,
+                 uint32_t* d_words, uint32_t* d_vstart, uint32_t* d_values,
+                 void* d_scratch, uint32_t epoch, void* stream);
+int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart,
+                  uint64_t n, const void* d_ctl, uint32_t* d_entries,
+                  void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Device primitives behind the reference's public WAH device API
+ * (p/core/include/ndactor/wah_device.hpp:17-50).
+ * ------------------------------------------------------------------------- */
+/* scan_exclusive (wah_scan.cpp:14-95): out[i] = sum(in[0..i)) mod 2^32. */
+size_t ndx_scan_scratch_bytes(uint64_t n);
+int ndx_scan_exclusive_u32(const uint32_t* d_in, uint32_t* d_out, uint64_t n,
+                           void* d_scratch, uint32_t epoch, void* stream);
+
+/* sort_pairs (wah_radix.cpp:16-127): stable by key, in place. */
+size_t ndx_sort_pairs_scratch_bytes(uint64_t n);
+int ndx_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_payloads, uint64_t n,
+                       void* d_scratch, uint32_t epoch, void* stream);
+
+/* The three compaction stages (wah_stages.cpp:29-163), same protocol:
+ * cfg is u32[2]; cfg[0] = k on the way in, cfg[1] = output length. */
+int ndx_compact_prepare(uint32_t* d_cfg, const uint32_t* d_a,
+                        const uint32_t* d_b, uint64_t k, uint32_t* d_out,
+                        void* stream);
+/* counts[t] = nonzeros in data[4096 t, 4096 t + 4096) (wah_stages.cpp:59-91) */
+int ndx_compact_count(const uint32_t* d_data, uint64_t n, uint32_t* d_counts,
+                      void* stream);
+/* order-preserving scatter of nonzeros; cfg[1] = total (wah_stages.cpp:93-156) */
+size_t ndx_compact_move_scratch_bytes(uint64_t n);
+int ndx_compact_move(uint32_t* d_cfg, const uint32_t* d_data, uint64_t n,
+                     const uint32_t* d_counts, uint32_t* d_out,
+                     void* d_scratch, uint32_t epoch, void* stream);
+
+/* One-CTA, one-warp `p[0] += 1` kernel: the dispatch-overhead probe of
+ * BASELINE config 2 (p/benchmarks/bench_device.cpp:14-24). */
+int ndx_tiny_increment(uint32_t* d_p, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NDX_H */

@@ -1,0 +1,155 @@
+"""GPU parity: the sm_100a build (through the C ABI, include/ndx.h) against the
+oracle and the reference-generated golden fixtures.  Bit-exact, no tolerance.
+
+Mirrors p/tests/test_wah_device.cpp:45-274 and acceptance.cpp checks 1-3."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1709_07781_b200 import gen
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def same(got, want):
+    return got.row_count == want.row_count and np.array_equal(got.entries, want.entries) and \
+        np.array_equal(got.words, want.words)
+
+
+def test_small_golden_cases(builder, port):
+    z = np.load(os.path.join(GOLD, "small_cases.npz"))
+    for k in z.files:
+        if not k.startswith("in_"):
+            continue
+        name = k[3:]
+        v = z[k]
+        got = builder.build(v)
+        import oracle
+
+        ser = oracle.Index(got.row_count, got.entries, got.words).serialize()
+        assert ser == z["out_" + name].tobytes(), name
+
+
+def test_random_instances_across_cardinalities(builder, port):  # test_wah_device.cpp:202-216
+    rng = np.random.default_rng(8005)
+    for it in range(24):
+        n = int(rng.integers(1, 30001))
+        card = [1, 2, 10, 1000][it % 4]
+        v = (rng.integers(0, card, n).astype(np.uint32) * 37 + 11)
+        assert same(builder.build(v), port.reference_index(v)), (it, n, card)
+
+
+def test_clustered_rows_produce_ones_fills(builder, port):  # test_wah_device.cpp:218-230
+    v = np.repeat(np.arange(200) % 3, 150).astype(np.uint32)
+    got = builder.build(v)
+    assert same(got, port.reference_index(v))
+    assert any((w & 0xC0000000) == 0xC0000000 for w in got.words.tolist())
+
+
+def test_single_row_and_empty(builder, port):  # test_wah_device.cpp:232-244
+    got = builder.build(np.array([77], np.uint32))
+    assert got.words.tolist() == [1] and got.entries.tolist() == [[77, 0, 1]]
+    e = builder.build(np.zeros(0, np.uint32))
+    assert e.row_count == 0 and e.entries.size == 0 and e.words.size == 0
+
+
+@pytest.mark.parametrize("case", ["long_stretch", "stretch_tile_edges", "sorted_blocks", "mode_edges",
+                                  "full_range", "hi_bytes", "constant", "two_values_alt"])
+def test_adversarial_shapes(builder, port, case):
+    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    if case == "long_stretch":  # ones-stretches spanning many emit tiles
+        v = np.repeat(np.array([3, 1, 4, 1, 5], np.uint32), [200_000, 31 * 5000, 93, 31 * 777 + 5, 10])
+    elif case == "stretch_tile_edges":
+        parts = []
+        for L in [31 * 132 - 1, 31 * 132, 31 * 132 + 1, 4096, 4095, 8192 + 31, 62, 30, 31]:
+            parts.append(np.full(L, len(parts) % 4, np.uint32))
+        v = np.concatenate(parts * 20)
+    elif case == "sorted_blocks":
+        v = np.sort(rng.integers(0, 5000, 300_000)).astype(np.uint32)
+    elif case == "mode_edges":  # key range 2047 / 2048 / 2049 (wide vs byte passes)
+        v = np.concatenate([rng.integers(10, 10 + r, 40_000) for r in (2047, 2048, 2049)]).astype(np.uint32)
+    elif case == "full_range":  # all four byte passes
+        v = rng.integers(0, 2**32, 200_000, dtype=np.uint64).astype(np.uint32)
+        v[3] = 0xFFFFFFFF
+        v[100] = 0x80000000
+    elif case == "hi_bytes":  # bytes 2/3 vary, 0/1 constant
+        v = (rng.integers(0, 300, 100_000).astype(np.uint32) << 16) | 0x1234
+    elif case == "constant":
+        v = np.full(123_457, 0xFFFFFFFF, np.uint32)
+    else:
+        v = np.tile(np.array([0xAAAA, 0x5555], np.uint32), 70_001)
+    got = builder.build(v)
+    want = port.reference_index(v)
+    assert same(got, want), case
+
+
+def _digests():
+    with open(os.path.join(GOLD, "digests.json")) as f:
+        return json.load(f)
+
+
+def test_acceptance_instances(builder, port):  # acceptance.cpp:56-79 (check 1)
+    a = _digests()["acceptance"]
+    inst = gen.instances(a["seed"], a["count"], a["cards"], a["max_rows"])
+    for i, (v, d) in enumerate(zip(inst, a["digests"])):
+        got = builder.build(v)
+        assert "%016x" % port.digest_parts(got.row_count, got.entries, got.words) == d, i
+
+
+@pytest.mark.parametrize("w", _digests()["workloads"], ids=lambda w: f"{w['kind']}-n{w['n']}-k{w['k']}")
+def test_baseline_workload_digests(builder, port, w):
+    """C1, C3, C4 and friends: digest of serialize_index equals the reference's."""
+    v = gen.uniform(w["seed"], w["n"], w["k"]) if w["kind"] == "uniform" else gen.zipf(w["seed"], w["n"], w["k"], w["s"])
+    got = builder.build(v)
+    assert got.words.size == w["W"] and len(got.entries) == w["D"]
+    assert "%016x" % port.digest_parts(got.row_count, got.entries, got.words) == w["digest"]
+
+
+def test_repeat_builds_are_deterministic(builder, port):
+    v = gen.uniform(3, 500_000, 300)
+    a = builder.build(v)
+    for _ in range(3):
+        assert same(builder.build(v), a)
+    assert same(a, port.reference_index(v))
+
+
+# ---- device primitives behind the reference's public API -----------------
+
+@pytest.mark.parametrize("n", [1, 2, 1023, 1024, 1025, 4096, 50000, 1048577])
+def test_scan_matches_serial_oracle(prims, port, n):  # test_wah_device.cpp:45-61
+    x = np.random.default_rng(n).integers(0, 10, n).astype(np.uint32)
+    assert np.array_equal(prims.scan_exclusive(x), port.scan_exclusive(x))
+
+
+def test_scan_wraps_mod_2_32(prims, port):
+    x = np.full(100_000, 0xFFFFFFF0, np.uint32)
+    assert np.array_equal(prims.scan_exclusive(x), port.scan_exclusive(x))
+
+
+@pytest.mark.parametrize("n", [1, 7, 16384, 16385, 40000])
+def test_sort_pairs_stable(prims, port, n):  # test_wah_device.cpp:63-107
+    rng = np.random.default_rng(8002 + n)
+    keys = rng.integers(0, 6, n).astype(np.uint32)
+    if n > 20:
+        keys[3] = 0xFFFFFFFF
+        keys[n // 2] = 0x80000000
+    pos = np.arange(n, dtype=np.uint32)
+    k, p = prims.sort_pairs(keys, pos)
+    ek, ep = port.sort_pairs(keys, pos)
+    assert np.array_equal(k, ek) and np.array_equal(p, ep)
+
+
+def test_compaction_drops_zeros_keeps_order(prims, port):  # test_wah_device.cpp:109-133, acceptance 3
+    rng = np.random.default_rng(8003)
+    for it in range(60):
+        n = int(rng.integers(1, 20001))
+        if it % 10 == 8:
+            x = np.zeros(n, np.uint32)
+        elif it % 10 == 9:
+            x = rng.integers(1, 100, n).astype(np.uint32)
+        else:
+            x = rng.integers(0, 3, n).astype(np.uint32)
+        assert np.array_equal(prims.compact(x), port.filter_nonzero(x)), it

@@ -1,0 +1,70 @@
+"""Per-stage device timing of the 4-stage build (CUDA events on the launch
+stream), for iteration on the kernels.  Usage:
+    python tools/stage_times.py [C3|C4|C1] [--reps 10] [--check]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1709_07781_b200 import gen, ndx  # noqa: E402
+from paper_1709_07781_b200.ndx import _ptr, check  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", nargs="?", default="C3")
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    v = gen.config_values(a.config, a.n or None)
+    n = v.size
+    b = ndx.WahBuilder(n)
+    keys = torch.from_numpy(v.view(np.int32)).cuda()
+    s = torch.cuda.current_stream()
+    sh = s.cuda_stream
+    L = b.lib
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    flush = torch.empty(256 << 20, dtype=torch.int32, device="cuda")
+    times = []
+    for rep in range(a.reps + 3):
+        flush.zero_()
+        ep = b._next_epoch()
+        ev[0].record(s)
+        check(L.ndx_wah_plan(_ptr(keys), n, _ptr(b.ctl), sh))
+        ev[1].record(s)
+        check(L.ndx_wah_sort(_ptr(keys), n, 0, _ptr(b.ctl), _ptr(b.pairs), _ptr(b.sort_scr), ep, sh))
+        ev[2].record(s)
+        check(L.ndx_wah_emit(_ptr(b.pairs), n, _ptr(b.ctl), _ptr(b.words), _ptr(b.vstart), _ptr(b.values),
+                             _ptr(b.emit_scr), ep, sh))
+        ev[3].record(s)
+        check(L.ndx_wah_table(_ptr(b.values), _ptr(b.vstart), n, _ptr(b.ctl), _ptr(b.entries), sh))
+        ev[4].record(s)
+        torch.cuda.synchronize()
+        if rep >= 3:
+            times.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
+    t = np.median(np.array(times), axis=0)
+    W, D = b.counts()
+    tot = t.sum()
+    print(f"{a.config} n={n} W={W} D={D}")
+    for name, x in zip(["plan", "sort", "emit", "table"], t):
+        print(f"  {name:6s} {x * 1e3:9.1f} us")
+    balg = 40 * n + 4 * W + 12 * D
+    print(f"  total  {tot * 1e3:9.1f} us  -> {n / tot / 1e6:.2f} G values/s, "
+          f"{balg / tot / 1e6:.0f} GB/s on the 40N+4W+12D model")
+    if a.check:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import oracle
+
+        got = b.fetch(n)
+        d = oracle.Port().digest_parts(got.row_count, got.entries, got.words)
+        print("  digest %016x" % d)
+
+
+if __name__ == "__main__":
+    main()
