@@ -76,17 +76,20 @@ int ndx_memcpy_d2d_async(void* d_dst, const void* d_src, size_t bytes, void* str
  * WAH index build: the four device stages.
  * Replaces wah::build_index (p/core/src/wah_builder.cpp:38-307).
  *
- *   S1 plan   keys[n]            -> ctl (histograms, key range, sort plan)
- *   S2 sort   keys[n] + ctl      -> pairs[n]  (stable by key; row ids made on the fly)
- *   S3 emit   pairs[n] + ctl     -> words[<=2n], vstart[<=n], values[<=n], ctl.{words,distinct}
- *   S4 table  values, vstart     -> entries[3*D] (value, offset, length)
+ *   S1 plan   keys[n]              -> ctl (key range, histograms, sort plan)
+ *   S2 sort   keys[n] + ctl        -> pairs[n]: u64 (key | row << 32), stable
+ *                                     by key; row ids made on the fly
+ *   S3 emit   pairs + ctl          -> words[<=2n], vstart[<=n], values[<=n],
+ *                                     ctl.{words, distinct}
+ *   S4 table  values, vstart, ctl  -> entries[3*D] (value, offset, length)
  *
  * `ctl` is a device block of ndx_wah_ctl_bytes() bytes; its first 24 bytes
- * are an ndx_wah_counts the host may read back after S3.
- * Scratch buffers must be zero-filled once after allocation.  `epoch` is a
- * caller-managed counter: each build must use a value not used with the same
- * scratch since it was last zeroed; a build consumes epoch .. epoch+7.
- * n must be below 2^31 (the word offsets of the index format are u32).
+ * are an ndx_wah_counts the host may read back after S3.  `status` is a
+ * buffer of ndx_wah_status_bytes(n) bytes owned by the caller, zero-filled
+ * ONCE after allocation and used for nothing else: it carries the sort's
+ * decoupled look-back statuses, tagged per build so it never needs
+ * clearing.  All sizes stay on the device: no stage needs a host round trip.
+ * n must be below 2^31 (the index format's word offsets are u32).
  * ------------------------------------------------------------------------- */
 typedef struct {
   uint64_t words;     /* W: compressed words in the index         */
@@ -96,16 +99,16 @@ typedef struct {
 } ndx_wah_counts;
 
 size_t ndx_wah_ctl_bytes(void);
-size_t ndx_wah_sort_scratch_bytes(uint64_t n);
+size_t ndx_wah_status_bytes(uint64_t n);
 size_t ndx_wah_emit_scratch_bytes(uint64_t n);
 
-int ndx_wah_plan(const uint32_t* d_keys, uint64_t n, void* d_ctl, void* stream);
-int ndx_wah_sort(const uint32_t* d_keys, uint64_t n, uint32_t row_base,
-                 void* d_ctl, uint64_t* d_pairs, void* d_scratch,
-                 uint32_t epoch, void* stream);
-int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl,
-                 uint32_t* d_words, uint32_t* d_vstart, uint32_t* d_values,
-                 void* d_scratch, uint32_t epoch, void* stream);
+int ndx_wah_plan(const uint32_t* d_keys, uint64_t n, void* d_ctl, void* d_status,
+                 void* stream);
+int ndx_wah_sort(const uint32_t* d_keys, uint64_t n, uint32_t row_base, void* d_ctl,
+                 uint64_t* d_pairs, uint64_t* d_tmp_pairs, void* d_status, void* stream);
+int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl, uint32_t* d_words,
+                 uint32_t* d_vstart, uint32_t* d_values, void* d_emit_scratch,
+                 void* stream);
 int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart,
                   uint64_t n, const void* d_ctl, uint32_t* d_entries,
                   void* stream);
@@ -117,12 +120,12 @@ int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart,
 /* scan_exclusive (wah_scan.cpp:14-95): out[i] = sum(in[0..i)) mod 2^32. */
 size_t ndx_scan_scratch_bytes(uint64_t n);
 int ndx_scan_exclusive_u32(const uint32_t* d_in, uint32_t* d_out, uint64_t n,
-                           void* d_scratch, uint32_t epoch, void* stream);
+                           void* d_scratch, void* stream);
 
 /* sort_pairs (wah_radix.cpp:16-127): stable by key, in place. */
 size_t ndx_sort_pairs_scratch_bytes(uint64_t n);
 int ndx_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_payloads, uint64_t n,
-                       void* d_scratch, uint32_t epoch, void* stream);
+                       void* d_scratch, void* stream);
 
 /* The three compaction stages (wah_stages.cpp:29-163), same protocol:
  * cfg is u32[2]; cfg[0] = k on the way in, cfg[1] = output length. */
@@ -136,7 +139,7 @@ int ndx_compact_count(const uint32_t* d_data, uint64_t n, uint32_t* d_counts,
 size_t ndx_compact_move_scratch_bytes(uint64_t n);
 int ndx_compact_move(uint32_t* d_cfg, const uint32_t* d_data, uint64_t n,
                      const uint32_t* d_counts, uint32_t* d_out,
-                     void* d_scratch, uint32_t epoch, void* stream);
+                     void* d_scratch, void* stream);
 
 /* One-CTA, one-warp `p[0] += 1` kernel: the dispatch-overhead probe of
  * BASELINE config 2 (p/benchmarks/bench_device.cpp:14-24). */

@@ -19,7 +19,6 @@ namespace ndx {
 constexpr uint32_t kStageTile = 4096;  // wah_stages.cpp:11 (counts are per tile)
 constexpr int kCThreads = 256;
 constexpr int kCWarps = kCThreads / 32;
-constexpr int kCRounds = kStageTile / kCThreads;  // 16 rounds of 32 per warp
 
 // prepare: out[2i] = a[i], out[2i+1] = b[i]; cfg[1] = 2k (wah_stages.cpp:36-46).
 __global__ void k_prepare(uint32_t* __restrict__ cfg, const uint32_t* __restrict__ a,
@@ -248,8 +247,7 @@ size_t ndx_compact_move_scratch_bytes(uint64_t n) {
 }
 
 int ndx_compact_move(uint32_t* d_cfg, const uint32_t* d_data, uint64_t n,
-                     const uint32_t* d_counts, uint32_t* d_out, void* d_scratch, uint32_t epoch,
-                     void* stream) {
+                     const uint32_t* d_counts, uint32_t* d_out, void* d_scratch, void* stream) {
   if (!d_cfg || !d_counts || !d_scratch || (n && (!d_data || !d_out))) return NDX_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int sms = 0;
@@ -258,18 +256,18 @@ int ndx_compact_move(uint32_t* d_cfg, const uint32_t* d_data, uint64_t n,
   const uint64_t tiles = stage_tiles(n > 0 ? n : 1);
   uint32_t* ctr = reinterpret_cast<uint32_t*>(static_cast<char*>(d_scratch));
   uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<char*>(d_scratch) + 256);
-  cudaError_t e = cudaMemsetAsync(ctr, 0, 4, s);
+  // counter + statuses cleared per call (status epoch 1 then means "this call")
+  cudaError_t e = cudaMemsetAsync(ctr, 0, 256 + tiles * 8, s);
   if (e) return e;
   const int grid = int(umin<uint64_t>(tiles, uint64_t(sms) * 8));
-  k_move<<<grid, kCThreads, 0, s>>>(d_cfg, d_data, n, d_counts, d_out, tiles, status, ctr,
-                                    epoch & 0xffffu);
+  k_move<<<grid, kCThreads, 0, s>>>(d_cfg, d_data, n, d_counts, d_out, tiles, status, ctr, 1u);
   return cudaGetLastError();
 }
 
 size_t ndx_scan_scratch_bytes(uint64_t n) { return size_t(stage_tiles(n) + 1) * 8 + 256; }
 
 int ndx_scan_exclusive_u32(const uint32_t* d_in, uint32_t* d_out, uint64_t n, void* d_scratch,
-                           uint32_t epoch, void* stream) {
+                           void* stream) {
   if (n == 0) return 0;
   if (!d_in || !d_out || !d_scratch) return NDX_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -279,10 +277,10 @@ int ndx_scan_exclusive_u32(const uint32_t* d_in, uint32_t* d_out, uint64_t n, vo
   const uint64_t tiles = stage_tiles(n);
   uint32_t* ctr = reinterpret_cast<uint32_t*>(static_cast<char*>(d_scratch));
   uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<char*>(d_scratch) + 256);
-  cudaError_t e = cudaMemsetAsync(ctr, 0, 4, s);
+  cudaError_t e = cudaMemsetAsync(ctr, 0, 256 + tiles * 8, s);
   if (e) return e;
   const int grid = int(umin<uint64_t>(tiles, uint64_t(sms) * 8));
-  k_scan<<<grid, kCThreads, 0, s>>>(d_in, d_out, n, tiles, status, ctr, epoch & 0xffffu);
+  k_scan<<<grid, kCThreads, 0, s>>>(d_in, d_out, n, tiles, status, ctr, 1u);
   return cudaGetLastError();
 }
 

@@ -45,8 +45,7 @@ __device__ uint32_t stretch_end(const uint64_t* __restrict__ pairs, uint64_t n, 
     if (g + t >= n) return false;
     uint64_t rr = uint64_t(row) + t;
     if (rr > 0xffffffffull) return false;
-    uint64_t e = pairs[g + t];
-    return pkey(e) == v && prow(e) == uint32_t(rr);
+    return pairs[g + t] == (uint64_t(v) | (rr << 32));
   };
   uint64_t lo = 30, hi, step = 32;
   for (;;) {
@@ -68,33 +67,34 @@ __device__ uint32_t stretch_end(const uint64_t* __restrict__ pairs, uint64_t n, 
   return uint32_t(lo);
 }
 
-struct EmitScratch {
-  uint64_t* val_agg;
-  uint64_t* val_pre;
-  uint32_t* status;
-};
+// Static round-robin tiles: CTA c takes tiles c, c+G, c+2G, ...  A tile's
+// global offsets are the CTA's own previous tile's offsets plus the
+// aggregates of the G tiles in between -- one block-wide read of G
+// published aggregates, never a chain of look-backs.  All G CTAs must be
+// co-resident (cooperative launch); every dependency is on a smaller tile
+// index and aggregates are published before waiting, so it cannot deadlock.
+constexpr uint64_t kAggReady = 1ull << 63;
 
 __global__ __launch_bounds__(kEmitThreads) void k_emit(const uint64_t* __restrict__ pairs,
                                                        uint64_t n, Ctl* ctl,
                                                        uint32_t* __restrict__ words,
                                                        uint32_t* __restrict__ vstart,
                                                        uint32_t* __restrict__ values,
-                                                       EmitScratch sc, uint32_t epoch_in) {
+                                                       uint64_t* agg) {
   extern __shared__ __align__(16) unsigned char emit_smem[];
-  uint64_t* win = reinterpret_cast<uint64_t*>(emit_smem);       // [kEmitTile + 2 kHalo]
+  uint64_t* win = reinterpret_cast<uint64_t*>(emit_smem);                   // [kEmitTile + 2 kHalo]
   uint32_t* ow = reinterpret_cast<uint32_t*>(win + kEmitTile + 2 * kHalo);  // [2 kEmitTile]
   __shared__ uint32_t warp_tot[kEmitWarps];
-  __shared__ uint32_t s_tile, s_w0, s_d0, s_tot;
+  __shared__ uint32_t red_w[kEmitWarps], red_d[kEmitWarps];
+  __shared__ uint32_t s_tot;
 
-  const uint32_t epoch = (epoch_in + 6u) & 0xffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (n + kEmitTile - 1) / kEmitTile;
+  const uint64_t G = gridDim.x;
+  uint64_t prev_w = 0, prev_d = 0;  // this CTA's previous tile's exclusive offsets
+  int64_t prev_tile = -1;
 
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr[0], 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    if (tile >= ntiles) break;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += G) {
     const uint64_t tile_start = tile * kEmitTile;
     const uint32_t m = uint32_t(umin<uint64_t>(kEmitTile, n - tile_start));
 
@@ -166,22 +166,14 @@ __global__ __launch_bounds__(kEmitThreads) void k_emit(const uint64_t* __restric
       const uint32_t t = lane < kEmitWarps ? warp_tot[lane] : 0;
       const uint32_t ti = warp_incl_sum(t);
       if (lane < kEmitWarps) warp_tot[lane] = ti - t;
-      const uint32_t tot = __shfl_sync(kFull, ti, 31);
-      if (lane == 0) {
-        s_tot = tot;
-        const uint64_t agg = uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32);
-        if (tile == 0) {
-          st_relaxed_u64(&sc.val_pre[0], agg);
-          st_release_u32(&sc.status[0], (epoch << 16) | 2u);
-        } else {
-          st_relaxed_u64(&sc.val_agg[tile], agg);
-          st_release_u32(&sc.status[tile], (epoch << 16) | 1u);
-        }
+      if (lane == 31) {
+        s_tot = ti;
+        st_relaxed_u64(&agg[tile], kAggReady | uint64_t(ti >> 16) | (uint64_t(ti & 0xffffu) << 32));
       }
     }
     __syncthreads();
 
-    // ---- stage the tile's words at tile-local offsets (no global offset needed)
+    // ---- stage the tile's words at tile-local offsets
     const uint32_t woff = warp_tot[warp];
 #pragma unroll
     for (int r = 0; r < kEmitIPT; ++r) {
@@ -192,50 +184,45 @@ __global__ __launch_bounds__(kEmitThreads) void k_emit(const uint64_t* __restric
       if (body[r]) ow[o] = body[r];
     }
 
-    // ---- decoupled look-back (warp 0) for the tile's global offsets
-    if (warp == 0) {
-      const uint32_t tot = s_tot;
-      const uint64_t agg = uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32);
-      uint64_t excl = 0;
-      if (tile > 0) {
-        int64_t base = int64_t(tile) - 1;
-        for (;;) {
-          const int64_t tt = base - lane;
-          uint64_t val = 0;
-          bool pre = true;
-          if (tt >= 0) {
-            uint32_t s = ld_acquire_u32(&sc.status[tt]);
-            while ((s >> 16) != epoch || (s & 3u) == 0) {
-              __nanosleep(20);
-              s = ld_acquire_u32(&sc.status[tt]);
-            }
-            pre = (s & 3u) == 2u;
-            val = pre ? ld_relaxed_u64(&sc.val_pre[tt]) : ld_relaxed_u64(&sc.val_agg[tt]);
-          }
-          const unsigned pm = __ballot_sync(kFull, pre);
-          if (pm && lane > __ffs(pm) - 1) val = 0;
-          excl += __shfl_sync(kFull, warp_incl_sum64(val), 31);
-          if (pm) break;
-          base -= 32;
-        }
-        if (lane == 0) {
-          st_relaxed_u64(&sc.val_pre[tile], excl + agg);
-          st_release_u32(&sc.status[tile], (epoch << 16) | 2u);
-        }
+    // ---- global offsets: previous tile of this CTA + aggregates in between
+    const uint64_t lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
+    uint32_t sw = 0, sd = 0;
+    for (uint64_t j = lo + threadIdx.x; j < tile; j += kEmitThreads) {
+      uint64_t s = ld_relaxed_u64(&agg[j]);
+      while (!(s & kAggReady)) {
+        __nanosleep(32);
+        s = ld_relaxed_u64(&agg[j]);
       }
-      if (lane == 0) {
-        s_w0 = uint32_t(excl);
-        s_d0 = uint32_t(excl >> 32);
-        if (tile == ntiles - 1) {
-          ctl->words = uint64_t(uint32_t(excl)) + (tot >> 16);
-          ctl->distinct = uint64_t(uint32_t(excl >> 32)) + (tot & 0xffffu);
-        }
-      }
+      sw += uint32_t(s);
+      sd += uint32_t(s >> 32) & 0x7fffffffu;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sw += __shfl_xor_sync(kFull, sw, o);
+      sd += __shfl_xor_sync(kFull, sd, o);
+    }
+    if (lane == 0) {
+      red_w[warp] = sw;
+      red_d[warp] = sd;
     }
     __syncthreads();
+    uint64_t w_add = 0, d_add = 0;
+#pragma unroll
+    for (int w = 0; w < kEmitWarps; ++w) {
+      w_add += red_w[w];
+      d_add += red_d[w];
+    }
+    const uint64_t W0 = prev_w + w_add, D0 = prev_d + d_add;
+    prev_w = W0;
+    prev_d = D0;
+    prev_tile = int64_t(tile);
+    const uint32_t tot = s_tot;
+    if (threadIdx.x == 0 && tile == ntiles - 1) {
+      ctl->words = W0 + (tot >> 16);
+      ctl->distinct = D0 + (tot & 0xffffu);
+    }
 
     // ---- table rows (value heads) straight to HBM
-    const uint32_t w0 = s_w0, d0 = s_d0;
 #pragma unroll
     for (int r = 0; r < kEmitIPT; ++r) {
       const uint32_t li = uint32_t(warp) * kEmitWarpItems + r * 32 + lane;
@@ -245,13 +232,13 @@ __global__ __launch_bounds__(kEmitThreads) void k_emit(const uint64_t* __restric
       const bool vhead = g == 0 || pkey(win[li + kHalo - 1]) != pkey(cur);
       if (vhead) {
         const uint32_t ex = woff + exw[r];
-        const uint32_t dd = d0 + (ex & 0xffffu);
-        vstart[dd] = w0 + (ex >> 16);
+        const uint64_t dd = D0 + (ex & 0xffffu);
+        vstart[dd] = uint32_t(W0 + (ex >> 16));
         values[dd] = pkey(cur);
       }
     }
-    const uint32_t tw = s_tot >> 16;
-    for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[uint64_t(w0) + j] = ow[j];
+    const uint32_t tw = tot >> 16;
+    for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[W0 + j] = ow[j];
     __syncthreads();
   }
 }
@@ -287,41 +274,38 @@ using namespace ndx;
 
 extern "C" {
 
-size_t ndx_wah_emit_scratch_bytes(uint64_t n) {
-  const uint64_t t = emit_tiles(n) + 1;
-  return size_t(t) * (8 + 8 + 4) + 1024;
-}
+size_t ndx_wah_emit_scratch_bytes(uint64_t n) { return size_t(emit_tiles(n) + 1) * 8 + 256; }
 
 int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl, uint32_t* d_words,
-                 uint32_t* d_vstart, uint32_t* d_values, void* d_scratch, uint32_t epoch,
-                 void* stream) {
+                 uint32_t* d_vstart, uint32_t* d_values, void* d_scratch, void* stream) {
   if (!d_pairs || !d_ctl || !d_words || !d_vstart || !d_values || !d_scratch || n == 0)
     return NDX_E_INVALID;
   if (n >= (1ull << 31)) return NDX_E_TOO_LARGE;
-  int sms = 0;
-  int rc = sm_count(&sms);
-  if (rc) return rc;
-  const uint64_t t = emit_tiles(n) + 1;
-  EmitScratch sc;
-  sc.val_agg = static_cast<uint64_t*>(d_scratch);
-  sc.val_pre = sc.val_agg + t;
-  sc.status = reinterpret_cast<uint32_t*>(sc.val_pre + t);
-  static bool attr_set[64] = {};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kEmitSmem));
-    if (e) return e;
-    attr_set[dev & 63] = true;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  static int grid_for[64] = {};
+  if (!grid_for[dev & 63]) {
+    if ((e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kEmitSmem))))
+      return e;
+    int sms = 0, occ = 0;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, kEmitThreads,
+                                                           kEmitSmem)))
+      return e;
+    grid_for[dev & 63] = sms * (occ > 0 ? occ : 1);
   }
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, kEmitThreads, kEmitSmem);
-  if (occ < 1) occ = 1;
-  const int grid = int(umin<uint64_t>(emit_tiles(n), uint64_t(sms) * occ));
-  k_emit<<<grid, kEmitThreads, kEmitSmem, static_cast<cudaStream_t>(stream)>>>(
-      d_pairs, n, static_cast<Ctl*>(d_ctl), d_words, d_vstart, d_values, sc, epoch);
-  return cudaGetLastError();
+  const uint64_t tiles = emit_tiles(n);
+  uint64_t* agg = static_cast<uint64_t*>(d_scratch);
+  if ((e = cudaMemsetAsync(agg, 0, tiles * 8, s))) return e;
+  int grid = int(umin<uint64_t>(tiles, uint64_t(grid_for[dev & 63])));
+  Ctl* ctl = static_cast<Ctl*>(d_ctl);
+  void* args[] = {(void*)&d_pairs, (void*)&n, (void*)&ctl,
+                  (void*)&d_words, (void*)&d_vstart, (void*)&d_values, (void*)&agg};
+  return cudaLaunchCooperativeKernel((const void*)k_emit, dim3(grid), dim3(kEmitThreads), args,
+                                     kEmitSmem, s);
 }
 
 int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart, uint64_t n,

@@ -21,6 +21,7 @@ struct SortPlan {
   uint32_t npasses;        // number of scatter passes that run
   uint32_t byte_active[4]; // bytes mode: byte k gets a pass
   uint32_t byte_order[4];  // bytes mode: execution index of byte k's pass
+  uint32_t byte_count[4];  // bytes mode: per-chunk histogram of byte k must be counted
   uint32_t bucket_start_wide[kWideBuckets];
   uint32_t bucket_start_byte[4][256];
 };
@@ -41,6 +42,7 @@ struct Ctl {
   uint32_t hist_wide[kWideBuckets];
   uint32_t zero_end;
   // ---- written by the plan kernel ----
+  uint32_t epoch;      // look-back status tag of this build (from the sort scratch counter)
   SortPlan plan;
 };
 

@@ -12,17 +12,20 @@
 //                   otherwise      -> byte-wise LSD passes over the bytes
 //                                     that vary (constant bytes skipped)
 //                 and turns the histograms into bucket start offsets.
-//   S2  k_onesweep<BITS>  persistent onesweep-style stable scatter: warp
-//                 ballot-match ranking, per-warp smem digit counters, a
-//                 decoupled look-back across tiles per digit, smem-staged
-//                 reordering so global stores are runs of consecutive pairs.
+//   S2  k_pass<BITS>  persistent onesweep-style stable scatter: tiles are
+//                 taken in global order from an atomic counter, the tile's
+//                 digit histogram is published before the ranking ("early
+//                 counts"), warp ballot-match ranking (lane order == row
+//                 order, so it is stable), a decoupled look-back per digit,
+//                 smem staging in digit order and a coalesced scatter of
+//                 runs.  Consecutive tiles in flight write adjacent parts of
+//                 every digit bucket, so partial sectors merge in L2.
 //                 The first pass synthesises row ids (no iota buffer).
-//                 Every pass kernel is launched unconditionally and exits at
-//                 once when the plan does not need it (no host sync).
+//   Every kernel is launched unconditionally and exits at once when the plan
+//   does not need it (no host synchronisation anywhere).
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
 
 #include "../../../include/ndx.h"
 #include "common.cuh"
@@ -30,19 +33,15 @@
 
 namespace ndx {
 
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortIPT = 16;                          // items per thread
+constexpr int kSortWarpItems = 32 * kSortIPT;         // 512
+constexpr int kSortTile = kSortThreads * kSortIPT;    // 4096 pairs
+
 // ------------------------------------------------------------------ S1 ----
 
-constexpr int kHistThreads = 1024;
-
-__device__ __forceinline__ void hist_one(uint32_t k, uint32_t* h0, uint32_t* h1,
-                                         uint32_t* hw, uint32_t& mx,
-                                         uint32_t& mxn) {
-  mx = max(mx, k);
-  mxn = max(mxn, ~k);
-  atomicAdd(&h0[k & 255u], 1u);
-  atomicAdd(&h1[(k >> 8) & 255u], 1u);
-  atomicAdd(&hw[k & (kWideBuckets - 1)], 1u);
-}
+constexpr int kHistThreads = 512;
 
 __global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restrict__ keys,
                                                        uint64_t n, Ctl* ctl) {
@@ -50,26 +49,36 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restric
   for (int i = threadIdx.x; i < 256; i += blockDim.x) h0[i] = h1[i] = 0;
   for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x) hw[i] = 0;
   __syncthreads();
-
   uint32_t mx = 0, mxn = 0;
+  auto one = [&](uint32_t k) {
+    mx = max(mx, k);
+    mxn = max(mxn, ~k);
+    atomicAdd(&h0[k & 255u], 1u);
+    atomicAdd(&h1[(k >> 8) & 255u], 1u);
+    atomicAdd(&hw[k & (kWideBuckets - 1)], 1u);
+  };
   const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   if ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0) {
-    const uint64_t nq = n / 4;
     const uint4* q = reinterpret_cast<const uint4*>(keys);
-    for (uint64_t i = tid; i < nq; i += stride) {
-      uint4 v = ldg_stream4(q + i);
-      hist_one(v.x, h0, h1, hw, mx, mxn);
-      hist_one(v.y, h0, h1, hw, mx, mxn);
-      hist_one(v.z, h0, h1, hw, mx, mxn);
-      hist_one(v.w, h0, h1, hw, mx, mxn);
+    const uint64_t nq = n / 4;
+    uint64_t i = tid;
+    for (; i + 3 * stride < nq; i += 4 * stride) {  // 4 loads in flight
+      const uint4 v0 = ldg_stream4(q + i), v1 = ldg_stream4(q + i + stride);
+      const uint4 v2 = ldg_stream4(q + i + 2 * stride), v3 = ldg_stream4(q + i + 3 * stride);
+      one(v0.x); one(v0.y); one(v0.z); one(v0.w);
+      one(v1.x); one(v1.y); one(v1.z); one(v1.w);
+      one(v2.x); one(v2.y); one(v2.z); one(v2.w);
+      one(v3.x); one(v3.y); one(v3.z); one(v3.w);
     }
-    for (uint64_t i = nq * 4 + tid; i < n; i += stride)
-      hist_one(keys[i], h0, h1, hw, mx, mxn);
+    for (; i < nq; i += stride) {
+      const uint4 v = ldg_stream4(q + i);
+      one(v.x); one(v.y); one(v.z); one(v.w);
+    }
+    for (uint64_t j = nq * 4 + tid; j < n; j += stride) one(keys[j]);
   } else {
-    for (uint64_t i = tid; i < n; i += stride) hist_one(keys[i], h0, h1, hw, mx, mxn);
+    for (uint64_t j = tid; j < n; j += stride) one(keys[j]);
   }
-  // warp-reduce the range, one atomic per warp
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mx = max(mx, __shfl_xor_sync(kFull, mx, o));
@@ -159,7 +168,10 @@ __device__ void plan_bytes(Ctl* ctl, uint64_t n, int nbytes) {
 }
 
 // stage 0: after k_hist; stage 1: after k_hist_hi (no-op unless pending).
-__global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage) {
+// `epoch_counter` lives in the status buffer's header; every build takes a
+// fresh tag so statuses of earlier builds never read as ready.
+__global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage,
+                                               uint32_t* epoch_counter) {
   SortPlan& p = ctl->plan;
   if (stage == 1) {
     if (p.complete) return;
@@ -170,6 +182,10 @@ __global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage) 
   __shared__ uint32_t rot[kWideBuckets];
   const uint32_t mn = ~ctl->max_not, mx = ctl->max_seen;
   if (threadIdx.x == 0) {
+    uint32_t ep = (*epoch_counter + 8u) & 0xfffff8u;
+    if (ep == 0) ep = 8;
+    *epoch_counter = ep;
+    ctl->epoch = ep;
     ctl->min_key = mn;
     ctl->max_key = mx;
     ctl->n_lo = uint32_t(n);
@@ -182,6 +198,7 @@ __global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage) 
       p.npasses = 1;
       p.complete = 1;
       p.need_hi = 0;
+      for (int k = 0; k < 4; ++k) p.byte_active[k] = 0;
     } else {
       p.mode = kModeBytes;
       p.need_hi = (mn >> 16) != (mx >> 16);
@@ -203,11 +220,60 @@ __global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage) 
 
 // ------------------------------------------------------------------ S2 ----
 
-constexpr int kSortThreads = 256;
-constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortIPT = 16;                          // items per thread
-constexpr int kSortWarpItems = 32 * kSortIPT;         // 512
-constexpr int kSortTile = kSortThreads * kSortIPT;    // 4096 pairs
+// Look-back status word: [63:40] epoch | [39:38] flag | [37:0] count.
+constexpr uint64_t kStAgg = 1ull << 38;
+constexpr uint64_t kStPrefix = 2ull << 38;
+constexpr uint64_t kStValue = (1ull << 38) - 1;
+
+__device__ __forceinline__ uint64_t st_word(uint32_t epoch, uint64_t flag, uint64_t v) {
+  return (uint64_t(epoch & 0xffffffu) << 40) | flag | v;
+}
+__device__ __forceinline__ bool st_ready(uint64_t s, uint32_t epoch) {
+  return uint32_t(s >> 40) == (epoch & 0xffffffu) && (s & (3ull << 38)) != 0;
+}
+
+struct SortArgs {
+  const uint32_t* in_keys;      // first pass: keys
+  const uint32_t* in_payloads;  // first pass: payloads, or null -> row ids synthesised
+  uint64_t* X;                  // final output pairs (the last pass writes X) ...
+  uint64_t* Y;                  // ... and the ping-pong buffer
+  uint32_t* out_keys;           // non-null: the last pass writes SoA here instead of X
+  uint32_t* out_payloads;
+  uint64_t n;
+  uint32_t row_base;
+  Ctl* ctl;
+  uint64_t* status;             // look-back statuses, tiles x 2048 words (own buffer)
+};
+
+struct PassInfo {
+  uint32_t shift, bits, base, epoch;
+  int p, P;
+  const uint32_t* bstart;
+};
+
+// The digit of pass `which` (-1 = wide); false if the pass does not run.
+__device__ __forceinline__ bool pass_info(const SortArgs& a, int which, PassInfo& pi) {
+  const SortPlan& pl = a.ctl->plan;
+  if (which < 0) {
+    if (pl.mode != kModeWide) return false;
+    pi.p = 0;
+    pi.P = 1;
+    pi.shift = 0;
+    pi.bits = pl.wide_bits;
+    pi.base = pl.base;
+    pi.bstart = pl.bucket_start_wide;
+  } else {
+    if (pl.mode != kModeBytes || !pl.byte_active[which]) return false;
+    pi.p = pl.byte_order[which];
+    pi.P = pl.npasses;
+    pi.shift = 8u * which;
+    pi.bits = 8;
+    pi.base = 0;
+    pi.bstart = pl.bucket_start_byte[which];
+  }
+  pi.epoch = a.ctl->epoch + uint32_t(which + 2);
+  return true;
+}
 
 template <int MAXB>
 struct SortSmem {
@@ -215,212 +281,258 @@ struct SortSmem {
   static constexpr size_t kHBytes = size_t(kSortWarps) * NB * sizeof(uint16_t);
   static constexpr size_t kSBytes = size_t(kSortTile) * sizeof(uint64_t);
   static constexpr size_t kUnion = kHBytes > kSBytes ? kHBytes : kSBytes;
-  static constexpr size_t kBytes = kUnion + 3 * NB * sizeof(uint32_t) + 16;
+  static constexpr size_t kBytes = kUnion + 2 * NB * sizeof(uint32_t) + 16;
 };
 
-struct SortArgs {
-  const uint32_t* in_keys;      // first pass: keys (SoA)
-  const uint32_t* in_payloads;  // first pass: payloads, or null -> rows synthesised
-  uint64_t* X;                  // final AoS output (or ping buffer)
-  uint64_t* Y;                  // pong buffer
-  uint32_t* out_keys;           // non-null: last pass writes SoA here
-  uint32_t* out_payloads;
-  uint64_t n;
-  uint32_t row_base;
-  Ctl* ctl;
-  uint64_t* status;             // look-back statuses, >= tiles * 2048 words
-  uint32_t epoch;
-};
-
-__device__ __forceinline__ uint64_t pack_pair(uint32_t key, uint32_t payload) {
-  return uint64_t(key) | (uint64_t(payload) << 32);
+// Lanes of the warp whose `BITS`-wide digit equals mine: per bit one
+// predicate, one ballot, one select, one 3-input logic op.
+template <int BITS>
+__device__ __forceinline__ unsigned warp_match(uint32_t d) {
+  unsigned peers = kFull;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t, m;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+        "selp.b32 m, 0, 0xffffffff, p;\n\t"
+        "xor.b32 t, t, m;\n\t"
+        "and.b32 %0, %0, t;\n\t}"
+        : "+r"(peers)
+        : "r"(d), "r"(1u << b));
+  }
+  return peers;
 }
 
-// which = -1: the wide single pass; which = 0..3: the byte-k pass.
-//
-// Per tile: load -> tile histogram (smem atomics) -> publish the per-digit
-// aggregates ("early counts", so successors rarely wait) -> stable warp
-// ranking -> look-back per digit -> stage the tile in digit order in smem ->
-// scatter runs of consecutive pairs.
-template <int MAXB>
-__global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(SortArgs a, int which) {
-  const SortPlan& pl = a.ctl->plan;
-  uint32_t shift, bits, base;
-  int p, P;
+struct TileCtx {
+  const uint32_t* in_keys;   // first pass (SoA) ...
+  const uint32_t* in_pays;   // ... payloads or null (row ids synthesised)
+  const uint64_t* in_pairs;  // later passes (AoS)
+  uint64_t* out_pairs;
+  uint32_t* out_keys;        // SoA output of the last pass (sort_pairs API)
+  uint32_t* out_pays;
+  uint32_t shift, base, row_base, epoch;
   const uint32_t* bstart;
-  if (which < 0) {
-    if (pl.mode != kModeWide) return;
-    p = 0;
-    P = 1;
-    shift = 0;
-    bits = pl.wide_bits;
-    base = pl.base;
-    bstart = pl.bucket_start_wide;
-  } else {
-    if (pl.mode != kModeBytes || !pl.byte_active[which]) return;
-    p = pl.byte_order[which];
-    P = pl.npasses;
-    shift = 8u * which;
-    bits = 8;
-    base = 0;
-    bstart = pl.bucket_start_byte[which];
+  uint64_t* status;
+  uint16_t* H;               // [warps][NB] per-warp digit counters (aliases S)
+  uint64_t* S;               // [tile] staging
+  uint32_t* cnt;             // [NB] tile count per digit
+  uint32_t* gbase;           // [NB] tile-local start, then global base - local start
+};
+
+// Exclusive count of digit d over all tiles before `tile` (decoupled
+// look-back, four predecessor statuses in flight at a time).
+__device__ __forceinline__ uint64_t lookback(const uint64_t* st, uint64_t tile, uint32_t nb,
+                                             uint32_t d, uint32_t epoch) {
+  uint64_t excl = 0;
+  int64_t t0 = int64_t(tile) - 1;
+  while (t0 >= 0) {
+    uint64_t s[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      s[j] = t0 - j >= 0 ? ld_relaxed_u64(&st[uint64_t(t0 - j) * nb + d]) : 0ull;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (t0 - j < 0) return excl;
+      while (!st_ready(s[j], epoch)) {
+        __nanosleep(64);
+        s[j] = ld_relaxed_u64(&st[uint64_t(t0 - j) * nb + d]);
+      }
+      excl += s[j] & kStValue;
+      if ((s[j] & (3ull << 38)) == kStPrefix) return excl;
+    }
+    t0 -= 4;
   }
-  const uint32_t nb = 1u << bits;
-  const uint32_t dmask = nb - 1;
-  const uint32_t epoch = a.epoch + uint32_t(which + 2);
+  return excl;
+}
 
-  // buffer roles: pass q writes X iff (P-1-q) is even
-  const bool first = p == 0, last = p == P - 1;
-  const uint64_t* in_pairs = first ? nullptr : (((P - 1 - (p - 1)) & 1) == 0 ? a.X : a.Y);
-  uint64_t* out_pairs = ((P - 1 - p) & 1) == 0 ? a.X : a.Y;
-  const bool out_soa = last && a.out_keys != nullptr;
-
-  extern __shared__ __align__(16) unsigned char smem[];
-  using SM = SortSmem<MAXB>;
-  uint16_t* H = reinterpret_cast<uint16_t*>(smem);       // [warps][NB]
-  uint64_t* S = reinterpret_cast<uint64_t*>(smem);       // [tile] (aliases H)
-  uint32_t* bh = reinterpret_cast<uint32_t*>(smem + SM::kUnion);  // tile histogram
-  uint32_t* tile_excl = bh + SM::NB;
-  uint32_t* gbase = tile_excl + SM::NB;
-  uint32_t* s_tile = gbase + SM::NB;
-
+// One tile of a stable scatter pass.  BITS is the digit width (compile
+// time, so the ballot match unrolls straight); FULL tiles skip every bounds
+// check.  Element order within a warp is round-major / lane-minor, which is
+// row order, so ranks taken round by round are stable.
+template <int BITS, int NBMAX, bool FULL>
+__device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint32_t tile_n) {
+  constexpr uint32_t NB = 1u << BITS;
+  constexpr uint32_t DMASK = NB - 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t n = a.n;
-  const uint64_t ntiles = (n + kSortTile - 1) / kSortTile;
-  uint32_t* ctr = &a.ctl->tile_ctr[which + 2];  // [0] emit, [1] wide, [2..5] bytes
-  uint16_t* Hw = H + warp * SM::NB;
+  const uint64_t tile_start = tile * kSortTile;
+  uint16_t* Hw = t.H + warp * NBMAX;
+  for (uint32_t d = lane; d < NB; d += 32) Hw[d] = 0;
+  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads) t.cnt[d] = 0;
 
+  const uint32_t wofs = uint32_t(warp) * kSortWarpItems + lane;
+  uint32_t key[kSortIPT], pay[kSortIPT];
+  if (t.in_pairs) {
+    const uint64_t* pp = t.in_pairs + tile_start + wofs;
+#pragma unroll
+    for (int r = 0; r < kSortIPT; ++r) {
+      const uint64_t e = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(pp + r * 32) : 0ull;
+      key[r] = uint32_t(e);
+      pay[r] = uint32_t(e >> 32);
+    }
+  } else {
+    const uint32_t* kp = t.in_keys + tile_start + wofs;
+#pragma unroll
+    for (int r = 0; r < kSortIPT; ++r)
+      key[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(kp + r * 32) : 0u;
+    if (t.in_pays) {
+      const uint32_t* rp = t.in_pays + tile_start + wofs;
+#pragma unroll
+      for (int r = 0; r < kSortIPT; ++r)
+        pay[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(rp + r * 32) : 0u;
+    } else {
+      const uint32_t r0 = t.row_base + uint32_t(tile_start) + wofs;
+#pragma unroll
+      for (int r = 0; r < kSortIPT; ++r) pay[r] = r0 + r * 32;
+    }
+  }
+  __syncthreads();
+
+  // ---- early counts: tile histogram, published before the heavy ranking
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r)
+    if (FULL || wofs + r * 32 < tile_n) atomicAdd(&t.cnt[((key[r] - t.base) >> t.shift) & DMASK], 1u);
+  __syncthreads();
+  uint64_t* st = t.status + tile * NB;
+  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads)
+    st_relaxed_u64(&st[d], st_word(t.epoch, tile == 0 ? kStPrefix : kStAgg, t.cnt[d]));
+
+  // ---- rank
+  uint32_t rank[kSortIPT];
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const uint32_t d = ((key[r] - t.base) >> t.shift) & DMASK;
+    unsigned peers = warp_match<BITS>(d);
+    bool valid = true;
+    if (!FULL) {
+      valid = wofs + r * 32 < tile_n;
+      peers &= __ballot_sync(kFull, valid);
+    }
+    const int leader = valid ? __ffs(peers) - 1 : lane;
+    uint32_t old = 0;
+    if (lane == leader) old = Hw[d];
+    old = __shfl_sync(kFull, old, leader);
+    if (valid && lane == leader) Hw[d] = uint16_t(old + __popc(peers));
+    rank[r] = old + __popc(peers & lanemask_lt());
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // ---- per digit: warp offsets (in place); tile-local digit starts
+  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const uint32_t c = t.H[w * NBMAX + d];
+      t.H[w * NBMAX + d] = uint16_t(sum);
+      sum += c;
+    }
+  }
+  block_excl_scan(t.cnt, t.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+
+  // ---- look-back: global base of each digit for this tile
+  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads) {
+    const uint32_t c = t.cnt[d], local = t.gbase[d];
+    uint64_t excl = 0;
+    if (tile > 0) {
+      excl = lookback(t.status, tile, NB, d, t.epoch);
+      st_relaxed_u64(&st[d], st_word(t.epoch, kStPrefix, excl + c));
+    }
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) t.H[w * NBMAX + d] += uint16_t(local);
+    t.gbase[d] = t.bstart[d] + uint32_t(excl) - local;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const uint32_t d = ((key[r] - t.base) >> t.shift) & DMASK;
+    rank[r] += Hw[d];
+  }
+  __syncthreads();  // H no longer read: S may overwrite it
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r)
+    if (FULL || wofs + r * 32 < tile_n) t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+  __syncthreads();
+
+  // ---- scatter: consecutive local slots of one digit are consecutive globally
+  const uint32_t lim = FULL ? uint32_t(kSortTile) : tile_n;
+  if (t.out_keys) {
+    for (uint32_t j = threadIdx.x; j < lim; j += kSortThreads) {
+      const uint64_t e = t.S[j];
+      const uint32_t pos = t.gbase[((uint32_t(e) - t.base) >> t.shift) & DMASK] + j;
+      t.out_keys[pos] = uint32_t(e);
+      t.out_pays[pos] = uint32_t(e >> 32);
+    }
+  } else {
+#pragma unroll 4
+    for (uint32_t j = threadIdx.x; j < lim; j += kSortThreads) {
+      const uint64_t e = t.S[j];
+      const uint32_t pos = t.gbase[((uint32_t(e) - t.base) >> t.shift) & DMASK] + j;
+      t.out_pairs[pos] = e;
+    }
+  }
+  __syncthreads();
+}
+
+template <int BITS, int NBMAX>
+__device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint32_t* s_tile,
+                                          uint64_t n) {
+  const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
   for (;;) {
     if (threadIdx.x == 0) *s_tile = atomicAdd(ctr, 1u);
-    for (uint32_t d = lane; d < nb; d += 32) Hw[d] = 0;
-    for (uint32_t d = threadIdx.x; d < nb; d += kSortThreads) bh[d] = 0;
     __syncthreads();
     const uint64_t tile = *s_tile;
-    if (tile >= ntiles) break;
-    const uint64_t tile_start = tile * kSortTile;
-    const uint32_t tile_n = uint32_t(umin<uint64_t>(kSortTile, n - tile_start));
-    const uint64_t wbase = tile_start + uint64_t(warp) * kSortWarpItems;
+    if (tile >= tiles) return;
+    const uint32_t tn = uint32_t(umin<uint64_t>(kSortTile, n - tile * kSortTile));
+    if (tn == uint32_t(kSortTile))
+      tile_pass<BITS, NBMAX, true>(t, tile, tn);
+    else
+      tile_pass<BITS, NBMAX, false>(t, tile, tn);
+  }
+}
 
-    // ---- load (warp-striped: round r, lane l -> element wbase + 32 r + l)
-    uint32_t key[kSortIPT], pay[kSortIPT];
-#pragma unroll
-    for (int r = 0; r < kSortIPT; ++r) {
-      const uint64_t i = wbase + uint64_t(r) * 32 + lane;
-      if (i < n) {
-        if (first) {
-          key[r] = ldg_stream(a.in_keys + i);
-          pay[r] = a.in_payloads ? ldg_stream(a.in_payloads + i) : a.row_base + uint32_t(i);
-        } else {
-          uint64_t e = ldg_stream(in_pairs + i);
-          key[r] = uint32_t(e);
-          pay[r] = uint32_t(e >> 32);
-        }
-      } else {
-        key[r] = 0;
-        pay[r] = 0;
-      }
-    }
-
-    // ---- early counts: tile histogram, published before the heavy ranking
-#pragma unroll
-    for (int r = 0; r < kSortIPT; ++r) {
-      const uint64_t i = wbase + uint64_t(r) * 32 + lane;
-      if (i < n) atomicAdd(&bh[((key[r] - base) >> shift) & dmask], 1u);
-    }
-    __syncthreads();
-    uint64_t* st = a.status + tile * nb;
-    for (uint32_t d = threadIdx.x; d < nb; d += kSortThreads)
-      st_relaxed_u64(&st[d], status_word(epoch, tile == 0 ? kFlagPrefix : kFlagAgg, bh[d]));
-
-    // ---- rank: stable within the warp (lane order == row order per round)
-    uint32_t rank[kSortIPT];
-#pragma unroll
-    for (int r = 0; r < kSortIPT; ++r) {
-      const uint64_t i = wbase + uint64_t(r) * 32 + lane;
-      const bool valid = i < n;
-      const unsigned vmask = __ballot_sync(kFull, valid);
-      const uint32_t d = ((key[r] - base) >> shift) & dmask;
-      unsigned peers = vmask;
-#pragma unroll
-      for (int b = 0; b < MAXB; ++b) {
-        if (b < int(bits)) {
-          unsigned bit = (d >> b) & 1u;
-          unsigned bal = __ballot_sync(kFull, bit);
-          peers &= bit ? bal : ~bal;
-        }
-      }
-      const int leader = valid ? __ffs(peers) - 1 : lane;
-      uint32_t old = 0;
-      if (valid && lane == leader) old = Hw[d];
-      old = __shfl_sync(kFull, old, leader);
-      if (valid && lane == leader) Hw[d] = uint16_t(old + __popc(peers));
-      rank[r] = old + __popc(peers & lanemask_lt());
-      __syncwarp();
-    }
-    __syncthreads();
-
-    // ---- per digit: warp offsets; tile-local digit offsets
-    for (uint32_t d = threadIdx.x; d < nb; d += kSortThreads) {
-      uint32_t sum = 0;
-#pragma unroll
-      for (int w = 0; w < kSortWarps; ++w) {
-        uint32_t c = H[w * SM::NB + d];
-        H[w * SM::NB + d] = uint16_t(sum);
-        sum += c;
-      }
-    }
-    block_excl_scan(bh, tile_excl, int(nb));  // ends with __syncthreads
-
-    // ---- decoupled look-back per digit
-    for (uint32_t d = threadIdx.x; d < nb; d += kSortThreads) {
-      const uint32_t cnt = bh[d];
-      uint64_t excl = 0;
-      if (tile > 0) {
-        int64_t t = int64_t(tile) - 1;
-        for (;;) {
-          uint64_t s = ld_relaxed_u64(&a.status[uint64_t(t) * nb + d]);
-          while (!status_ready(s, epoch)) {
-            __nanosleep(20);
-            s = ld_relaxed_u64(&a.status[uint64_t(t) * nb + d]);
-          }
-          excl += s & kValueMask;
-          if (status_is_prefix(s)) break;
-          --t;
-        }
-        st_relaxed_u64(&st[d], status_word(epoch, kFlagPrefix, excl + cnt));
-      }
-      gbase[d] = bstart[d] + uint32_t(excl) - tile_excl[d];
-    }
-    __syncthreads();
-
-    // ---- local (in-tile) positions, then stage the tile in smem
-#pragma unroll
-    for (int r = 0; r < kSortIPT; ++r) {
-      const uint32_t d = ((key[r] - base) >> shift) & dmask;
-      rank[r] += tile_excl[d] + Hw[d];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kSortIPT; ++r) {
-      const uint64_t i = wbase + uint64_t(r) * 32 + lane;
-      if (i < n) S[rank[r]] = pack_pair(key[r], pay[r]);
-    }
-    __syncthreads();
-
-    // ---- scatter: consecutive local slots of one digit are consecutive globally
-    for (uint32_t j = threadIdx.x; j < tile_n; j += kSortThreads) {
-      const uint64_t e = S[j];
-      const uint32_t k = uint32_t(e);
-      const uint32_t d = ((k - base) >> shift) & dmask;
-      const uint32_t pos = gbase[d] + j;
-      if (out_soa) {
-        a.out_keys[pos] = k;
-        a.out_payloads[pos] = uint32_t(e >> 32);
-      } else {
-        out_pairs[pos] = e;
-      }
-    }
-    __syncthreads();
+// One stable scatter pass over persistent CTAs.  Pass q writes X iff
+// (P-1-q) is even, so the last pass lands in X.
+template <int MAXB>
+__global__ __launch_bounds__(kSortThreads, 3) void k_pass(SortArgs a, int which) {
+  PassInfo pi;
+  if (!pass_info(a, which, pi)) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  using SM = SortSmem<MAXB>;
+  TileCtx t;
+  const bool first = pi.p == 0, last = pi.p == pi.P - 1;
+  t.in_keys = first ? a.in_keys : nullptr;
+  t.in_pays = first ? a.in_payloads : nullptr;
+  t.in_pairs = first ? nullptr : ((((pi.P - 1 - (pi.p - 1)) & 1) == 0) ? a.X : a.Y);
+  t.out_pairs = (((pi.P - 1 - pi.p) & 1) == 0) ? a.X : a.Y;
+  t.out_keys = last ? a.out_keys : nullptr;
+  t.out_pays = last ? a.out_payloads : nullptr;
+  t.shift = pi.shift;
+  t.base = pi.base;
+  t.row_base = a.row_base;
+  t.epoch = pi.epoch;
+  t.bstart = pi.bstart;
+  t.status = a.status;
+  t.H = reinterpret_cast<uint16_t*>(smem);
+  t.S = reinterpret_cast<uint64_t*>(smem);
+  t.cnt = reinterpret_cast<uint32_t*>(smem + SM::kUnion);
+  t.gbase = t.cnt + SM::NB;
+  uint32_t* s_tile = t.gbase + SM::NB;
+  uint32_t* ctr = &a.ctl->tile_ctr[which + 2];  // [0] emit, [1] wide, [2..5] bytes
+  if (MAXB == 8) {
+    tile_loop<8, SM::NB>(t, ctr, s_tile, a.n);
+  } else {
+    // digits above `bits` are zero for every key, so a wider match is exact
+    if (pi.bits <= 4)
+      tile_loop<4, SM::NB>(t, ctr, s_tile, a.n);
+    else if (pi.bits <= 8)
+      tile_loop<8, SM::NB>(t, ctr, s_tile, a.n);
+    else if (pi.bits <= 9)
+      tile_loop<9, SM::NB>(t, ctr, s_tile, a.n);
+    else if (pi.bits <= 10)
+      tile_loop<10, SM::NB>(t, ctr, s_tile, a.n);
+    else
+      tile_loop<(MAXB > 10 ? 11 : 10), SM::NB>(t, ctr, s_tile, a.n);
   }
 }
 
@@ -440,18 +552,18 @@ static int launch_cfg(LaunchCfg** out) {
   LaunchCfg& c = g_cfg[dev & 63];
   if (!c.ready) {
     if ((e = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-    size_t sw = SortSmem<kWideMaxBits>::kBytes, sb = SortSmem<8>::kBytes;
-    if ((e = cudaFuncSetAttribute(k_onesweep<kWideMaxBits>,
+    const size_t sw = SortSmem<kWideMaxBits>::kBytes, sb = SortSmem<8>::kBytes;
+    if ((e = cudaFuncSetAttribute(k_pass<kWideMaxBits>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw))))
       return e;
-    if ((e = cudaFuncSetAttribute(k_onesweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(k_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sb))))
       return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_wide, k_onesweep<kWideMaxBits>,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_wide, k_pass<kWideMaxBits>,
                                                            kSortThreads, sw)))
       return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_onesweep<8>,
-                                                           kSortThreads, sb)))
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_pass<8>, kSortThreads,
+                                                           sb)))
       return e;
     if (c.occ_wide < 1) c.occ_wide = 1;
     if (c.occ_byte < 1) c.occ_byte = 1;
@@ -463,6 +575,32 @@ static int launch_cfg(LaunchCfg** out) {
 
 static uint64_t sort_tiles(uint64_t n) { return (n + kSortTile - 1) / kSortTile; }
 
+static int launch_sort(SortArgs a, cudaStream_t s, LaunchCfg* c) {
+  const uint64_t tiles = sort_tiles(a.n);
+  const int gw = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_wide));
+  const int gb = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_byte));
+  k_pass<kWideMaxBits><<<gw, kSortThreads, SortSmem<kWideMaxBits>::kBytes, s>>>(a, -1);
+  for (int k = 0; k < 4; ++k) k_pass<8><<<gb, kSortThreads, SortSmem<8>::kBytes, s>>>(a, k);
+  return cudaGetLastError();
+}
+
+static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, uint32_t* epoch_counter,
+                       cudaStream_t s, LaunchCfg* c) {
+  cudaError_t e = cudaMemsetAsync(ctl, 0, offsetof(Ctl, zero_end), s);
+  if (e) return e;
+  const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * 4, (n + 65535) / 65536)));
+  k_hist<<<grid, kHistThreads, 0, s>>>(keys, n, ctl);
+  k_plan<<<1, 1024, 0, s>>>(ctl, n, 0, epoch_counter);
+  k_hist_hi<<<c->sms * 2, kHistThreads, 0, s>>>(keys, n, ctl);
+  k_plan<<<1, 1024, 0, s>>>(ctl, n, 1, epoch_counter);
+  return cudaGetLastError();
+}
+
+// Status buffer: [256 B header: u32 epoch counter][tiles x 2048 statuses]
+static size_t status_bytes(uint64_t n) {
+  return 256 + size_t(sort_tiles(n)) * kWideBuckets * sizeof(uint64_t);
+}
+
 }  // namespace ndx
 
 using namespace ndx;
@@ -471,69 +609,48 @@ extern "C" {
 
 size_t ndx_wah_ctl_bytes(void) { return (sizeof(Ctl) + 255) & ~size_t(255); }
 
-size_t ndx_wah_sort_scratch_bytes(uint64_t n) {
-  // look-back statuses (tiles x 2048 u64) + one pong buffer of pairs
-  size_t st = size_t(sort_tiles(n)) * kWideBuckets * sizeof(uint64_t);
-  st = (st + 255) & ~size_t(255);
-  return st + size_t(n) * sizeof(uint64_t) + 256;
-}
+size_t ndx_wah_status_bytes(uint64_t n) { return status_bytes(n); }
 
-int ndx_wah_plan(const uint32_t* d_keys, uint64_t n, void* d_ctl, void* stream) {
-  if (!d_keys || !d_ctl || n == 0) return NDX_E_INVALID;
+int ndx_wah_plan(const uint32_t* d_keys, uint64_t n, void* d_ctl, void* d_status,
+                 void* stream) {
+  if (!d_keys || !d_ctl || !d_status || n == 0) return NDX_E_INVALID;
   if (n >= (1ull << 31)) return NDX_E_TOO_LARGE;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   LaunchCfg* c;
   int rc = launch_cfg(&c);
   if (rc) return rc;
-  Ctl* ctl = static_cast<Ctl*>(d_ctl);
-  cudaError_t e = cudaMemsetAsync(ctl, 0, offsetof(Ctl, zero_end), s);
-  if (e) return e;
-  const uint64_t want = (n + 4ull * kHistThreads * 8 - 1) / (4ull * kHistThreads * 8);
-  const int grid = int(umin<uint64_t>(uint64_t(c->sms) * 2, umax<uint64_t>(want, 1)));
-  k_hist<<<grid, kHistThreads, 0, s>>>(d_keys, n, ctl);
-  k_plan<<<1, 1024, 0, s>>>(ctl, n, 0);
-  k_hist_hi<<<grid, kHistThreads, 0, s>>>(d_keys, n, ctl);
-  k_plan<<<1, 1024, 0, s>>>(ctl, n, 1);
-  return cudaGetLastError();
+  return launch_plan(d_keys, n, static_cast<Ctl*>(d_ctl), static_cast<uint32_t*>(d_status),
+                     static_cast<cudaStream_t>(stream), c);
 }
 
 int ndx_wah_sort(const uint32_t* d_keys, uint64_t n, uint32_t row_base, void* d_ctl,
-                 uint64_t* d_pairs, void* d_scratch, uint32_t epoch, void* stream) {
-  if (!d_keys || !d_ctl || !d_pairs || !d_scratch || n == 0) return NDX_E_INVALID;
+                 uint64_t* d_pairs, uint64_t* d_tmp_pairs, void* d_status, void* stream) {
+  if (!d_keys || !d_ctl || !d_pairs || !d_tmp_pairs || !d_status || n == 0)
+    return NDX_E_INVALID;
   if (n >= (1ull << 31)) return NDX_E_TOO_LARGE;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   LaunchCfg* c;
   int rc = launch_cfg(&c);
   if (rc) return rc;
-  const uint64_t tiles = sort_tiles(n);
-  size_t st = (size_t(tiles) * kWideBuckets * sizeof(uint64_t) + 255) & ~size_t(255);
   SortArgs a{};
   a.in_keys = d_keys;
-  a.in_payloads = nullptr;
   a.X = d_pairs;
-  a.Y = reinterpret_cast<uint64_t*>(static_cast<char*>(d_scratch) + st);
+  a.Y = d_tmp_pairs;
   a.n = n;
   a.row_base = row_base;
   a.ctl = static_cast<Ctl*>(d_ctl);
-  a.status = static_cast<uint64_t*>(d_scratch);
-  a.epoch = epoch;
-  const int gw = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_wide));
-  const int gb = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_byte));
-  k_onesweep<kWideMaxBits><<<gw, kSortThreads, SortSmem<kWideMaxBits>::kBytes, s>>>(a, -1);
-  for (int k = 0; k < 4; ++k)
-    k_onesweep<8><<<gb, kSortThreads, SortSmem<8>::kBytes, s>>>(a, k);
-  return cudaGetLastError();
+  a.status = reinterpret_cast<uint64_t*>(static_cast<char*>(d_status) + 256);
+  return launch_sort(a, static_cast<cudaStream_t>(stream), c);
 }
 
 size_t ndx_sort_pairs_scratch_bytes(uint64_t n) {
-  // ctl + statuses + pong pairs + ping pairs + SoA copies of the input
-  return ndx_wah_ctl_bytes() + ndx_wah_sort_scratch_bytes(n) + size_t(n) * 16 + 512;
+  // ctl | X pairs | Y pairs | copies of the input | statuses
+  return ndx_wah_ctl_bytes() + size_t(n) * 24 + status_bytes(n) + 1024;
 }
 
 // sort_pairs: stable sort of SoA (keys, payloads) in place.  The input is
-// copied aside first so the last pass can scatter into the caller's buffers.
+// copied aside so the last pass can scatter into the caller's buffers; the
+// status region is cleared per call (this entry point is not the hot path).
 int ndx_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_payloads, uint64_t n, void* d_scratch,
-                       uint32_t epoch, void* stream) {
+                       void* stream) {
   if (n == 0) return 0;
   if (!d_keys || !d_payloads || !d_scratch) return NDX_E_INVALID;
   if (n >= (1ull << 31)) return NDX_E_TOO_LARGE;
@@ -543,17 +660,16 @@ int ndx_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_payloads, uint64_t n, void*
   if (rc) return rc;
   char* base = static_cast<char*>(d_scratch);
   Ctl* ctl = reinterpret_cast<Ctl*>(base);
-  char* sort_scr = base + ndx_wah_ctl_bytes();
-  const uint64_t tiles = sort_tiles(n);
-  size_t st = (size_t(tiles) * kWideBuckets * sizeof(uint64_t) + 255) & ~size_t(255);
-  uint64_t* Y = reinterpret_cast<uint64_t*>(sort_scr + st);
-  uint64_t* X = Y + n;
-  uint32_t* ck = reinterpret_cast<uint32_t*>(X + n);
+  uint64_t* X = reinterpret_cast<uint64_t*>(base + ndx_wah_ctl_bytes());
+  uint64_t* Y = X + n;
+  uint32_t* ck = reinterpret_cast<uint32_t*>(Y + n);
   uint32_t* cp = ck + n;
+  char* status = reinterpret_cast<char*>(((reinterpret_cast<uintptr_t>(cp + n)) + 255) & ~uintptr_t(255));
   cudaError_t e;
+  if ((e = cudaMemsetAsync(status, 0, status_bytes(n), s))) return e;
   if ((e = cudaMemcpyAsync(ck, d_keys, n * 4, cudaMemcpyDeviceToDevice, s))) return e;
   if ((e = cudaMemcpyAsync(cp, d_payloads, n * 4, cudaMemcpyDeviceToDevice, s))) return e;
-  if ((rc = ndx_wah_plan(ck, n, ctl, stream))) return rc;
+  if ((rc = launch_plan(ck, n, ctl, reinterpret_cast<uint32_t*>(status), s, c))) return rc;
   SortArgs a{};
   a.in_keys = ck;
   a.in_payloads = cp;
@@ -563,14 +679,8 @@ int ndx_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_payloads, uint64_t n, void*
   a.out_payloads = d_payloads;
   a.n = n;
   a.ctl = ctl;
-  a.status = reinterpret_cast<uint64_t*>(sort_scr);
-  a.epoch = epoch;
-  const int gw = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_wide));
-  const int gb = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_byte));
-  k_onesweep<kWideMaxBits><<<gw, kSortThreads, SortSmem<kWideMaxBits>::kBytes, s>>>(a, -1);
-  for (int k = 0; k < 4; ++k)
-    k_onesweep<8><<<gb, kSortThreads, SortSmem<8>::kBytes, s>>>(a, k);
-  return cudaGetLastError();
+  a.status = reinterpret_cast<uint64_t*>(status + 256);
+  return launch_sort(a, s, c);
 }
 
 }  // extern "C"

@@ -55,26 +55,26 @@ SIGNATURES = [
     ("ndx_memcpy_d2h_async", ctypes.c_int, [_vp, _vp, _sz, _vp]),
     ("ndx_memcpy_d2d_async", ctypes.c_int, [_vp, _vp, _sz, _vp]),
     ("ndx_wah_ctl_bytes", _sz, []),
-    ("ndx_wah_sort_scratch_bytes", _sz, [_u64]),
+    ("ndx_wah_status_bytes", _sz, [_u64]),
     ("ndx_wah_emit_scratch_bytes", _sz, [_u64]),
-    ("ndx_wah_plan", ctypes.c_int, [_vp, _u64, _vp, _vp]),
-    ("ndx_wah_sort", ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _u32, _vp]),
-    ("ndx_wah_emit", ctypes.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _u32, _vp]),
+    ("ndx_wah_plan", ctypes.c_int, [_vp, _u64, _vp, _vp, _vp]),
+    ("ndx_wah_sort", ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp]),
+    ("ndx_wah_emit", ctypes.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ndx_wah_table", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_scan_scratch_bytes", _sz, [_u64]),
-    ("ndx_scan_exclusive_u32", ctypes.c_int, [_vp, _vp, _u64, _vp, _u32, _vp]),
+    ("ndx_scan_exclusive_u32", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     ("ndx_sort_pairs_scratch_bytes", _sz, [_u64]),
-    ("ndx_sort_pairs_u32", ctypes.c_int, [_vp, _vp, _u64, _vp, _u32, _vp]),
+    ("ndx_sort_pairs_u32", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     ("ndx_compact_prepare", ctypes.c_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
     ("ndx_compact_count", ctypes.c_int, [_vp, _u64, _vp, _vp]),
     ("ndx_compact_move_scratch_bytes", _sz, [_u64]),
-    ("ndx_compact_move", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _u32, _vp]),
+    ("ndx_compact_move", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     ("ndx_tiny_increment", ctypes.c_int, [_vp, _vp]),
 ]
 
 
 def lib_path() -> str:
-    return os.path.join(_build.LIB, "libndx.so")
+    return os.path.join(_build.LIB, os.environ.get("NDX_LIB", "libndx.so"))
 
 
 def load() -> ctypes.CDLL:
@@ -135,7 +135,6 @@ class WahBuilder:
         check(self.lib.ndx_device_open(device), "device_open")
         self.device = torch.device("cuda", device)
         self.capacity = 0
-        self.epoch = 8
         if capacity:
             self.ensure(capacity)
 
@@ -149,40 +148,38 @@ class WahBuilder:
             return
         L = self.lib
         self.ctl = self._alloc(L.ndx_wah_ctl_bytes(), zero=True)
-        self.sort_scr = self._alloc(L.ndx_wah_sort_scratch_bytes(n), zero=True)
-        self.emit_scr = self._alloc(L.ndx_wah_emit_scratch_bytes(n), zero=True)
+        self.status = self._alloc(L.ndx_wah_status_bytes(n), zero=True)  # zeroed once, statuses only
+        self.emit_scr = self._alloc(L.ndx_wah_emit_scratch_bytes(n))
         self.pairs = self._alloc(8 * n)
+        self.tmp_pairs = self._alloc(8 * n)
         self.words = self._alloc(8 * n)       # <= 2n words
         self.vstart = self._alloc(4 * n)
         self.values = self._alloc(4 * n)
         self.entries = self._alloc(12 * n)
         self.capacity = n
-        self.epoch = 8
 
-    def _next_epoch(self) -> int:
-        e = self.epoch
-        self.epoch += 8
-        if self.epoch >= 0x10000:  # statuses could alias an old epoch: clear
-            self.sort_scr.zero_()
-            self.emit_scr.zero_()
-            self.epoch = 8
-        return e
+    def stage_calls(self, keys, n: int, row_base: int = 0, stream=None):
+        """The four stage launches as callables (for per-stage timing)."""
+        L, s = self.lib, _stream_handle(stream)
+        return [
+            ("plan", lambda: check(L.ndx_wah_plan(_ptr(keys), n, _ptr(self.ctl), _ptr(self.status), s),
+                                   "wah_plan")),
+            ("sort", lambda: check(L.ndx_wah_sort(_ptr(keys), n, row_base, _ptr(self.ctl), _ptr(self.pairs),
+                                                  _ptr(self.tmp_pairs), _ptr(self.status), s), "wah_sort")),
+            ("emit", lambda: check(L.ndx_wah_emit(_ptr(self.pairs), n, _ptr(self.ctl), _ptr(self.words),
+                                                  _ptr(self.vstart), _ptr(self.values), _ptr(self.emit_scr), s),
+                                   "wah_emit")),
+            ("table", lambda: check(L.ndx_wah_table(_ptr(self.values), _ptr(self.vstart), n, _ptr(self.ctl),
+                                                    _ptr(self.entries), s), "wah_table")),
+        ]
 
     def launch(self, keys, n: int, row_base: int = 0, stream=None) -> None:
         """Enqueue S1..S4 on `stream` (no host synchronisation)."""
         self.ensure(n)
         if n == 0:
             return
-        L, s = self.lib, _stream_handle(stream)
-        ep = self._next_epoch()
-        check(L.ndx_wah_plan(_ptr(keys), n, _ptr(self.ctl), s), "wah_plan")
-        check(L.ndx_wah_sort(_ptr(keys), n, row_base, _ptr(self.ctl), _ptr(self.pairs),
-                             _ptr(self.sort_scr), ep, s), "wah_sort")
-        check(L.ndx_wah_emit(_ptr(self.pairs), n, _ptr(self.ctl), _ptr(self.words),
-                             _ptr(self.vstart), _ptr(self.values), _ptr(self.emit_scr), ep, s),
-              "wah_emit")
-        check(L.ndx_wah_table(_ptr(self.values), _ptr(self.vstart), n, _ptr(self.ctl),
-                              _ptr(self.entries), s), "wah_table")
+        for _, call in self.stage_calls(keys, n, row_base, stream):
+            call()
 
     def counts(self) -> tuple[int, int]:
         c = self.ctl[:6].cpu().numpy().view(np.uint64)
@@ -220,12 +217,6 @@ class Primitives:
         self.lib = load()
         check(self.lib.ndx_device_open(device), "device_open")
         self.device = torch.device("cuda", device)
-        self.epoch = 8
-
-    def _ep(self) -> int:
-        e = self.epoch
-        self.epoch = (self.epoch + 8) % 0xFFF8 or 8
-        return e
 
     def _dev(self, a: np.ndarray):
         a = np.ascontiguousarray(a, dtype=np.uint32)
@@ -244,7 +235,7 @@ class Primitives:
         d_out = self.torch.empty_like(d_in)
         scr = self.torch.zeros(self.lib.ndx_scan_scratch_bytes(n) // 4 + 64, dtype=self.torch.int32,
                                device=self.device)
-        check(self.lib.ndx_scan_exclusive_u32(_ptr(d_in), _ptr(d_out), n, _ptr(scr), self._ep(),
+        check(self.lib.ndx_scan_exclusive_u32(_ptr(d_in), _ptr(d_out), n, _ptr(scr),
                                               _stream_handle(None)), "scan")
         return self._host(d_out, n)
 
@@ -255,7 +246,7 @@ class Primitives:
         dk, dp = self._dev(keys), self._dev(payloads)
         scr = self.torch.zeros(self.lib.ndx_sort_pairs_scratch_bytes(n) // 4 + 64,
                                dtype=self.torch.int32, device=self.device)
-        check(self.lib.ndx_sort_pairs_u32(_ptr(dk), _ptr(dp), n, _ptr(scr), self._ep(),
+        check(self.lib.ndx_sort_pairs_u32(_ptr(dk), _ptr(dp), n, _ptr(scr),
                                           _stream_handle(None)), "sort_pairs")
         return self._host(dk, n), self._host(dp, n)
 
@@ -282,6 +273,6 @@ class Primitives:
         check(L.ndx_compact_prepare(_ptr(cfg), _ptr(da), _ptr(db), k, _ptr(inter), s), "prepare")
         check(L.ndx_compact_count(_ptr(inter), 2 * k, _ptr(counts), s), "count")
         check(L.ndx_compact_move(_ptr(cfg), _ptr(inter), 2 * k, _ptr(counts), _ptr(out),
-                                 _ptr(scr), self._ep(), s), "move")
+                                 _ptr(scr), s), "move")
         total = int(self._host(cfg, 2)[1])
         return self._host(out, total)

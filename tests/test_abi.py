@@ -45,7 +45,7 @@ def test_error_strings_and_sizes_without_gpu():
     assert b"invalid" in lib.ndx_error_string(10001)
     assert b"2^31" in lib.ndx_error_string(10002)
     assert lib.ndx_wah_ctl_bytes() % 256 == 0
-    assert lib.ndx_wah_sort_scratch_bytes(1 << 20) >= 8 * (1 << 20)
+    assert lib.ndx_wah_status_bytes(1 << 20) >= 2048 * 8 * 256
     assert lib.ndx_wah_emit_scratch_bytes(1 << 20) > 0
     assert lib.ndx_scan_scratch_bytes(5000) > 0
 
@@ -53,8 +53,8 @@ def test_error_strings_and_sizes_without_gpu():
 def test_launchers_validate_arguments_without_gpu():
     lib = ndx.load()
     # null pointers are rejected before any CUDA call
-    assert lib.ndx_wah_plan(None, 10, None, None) == 10001
-    assert lib.ndx_wah_emit(None, 10, None, None, None, None, None, 0, None) == 10001
+    assert lib.ndx_wah_plan(None, 10, None, None, None) == 10001
+    assert lib.ndx_wah_emit(None, 10, None, None, None, None, None, None) == 10001
     assert lib.ndx_compact_count(None, 5, None, None) == 10001
 
 

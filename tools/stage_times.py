@@ -32,19 +32,13 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     flush = torch.empty(256 << 20, dtype=torch.int32, device="cuda")
     times = []
+    calls = b.stage_calls(keys, n)
     for rep in range(a.reps + 3):
         flush.zero_()
-        ep = b._next_epoch()
         ev[0].record(s)
-        check(L.ndx_wah_plan(_ptr(keys), n, _ptr(b.ctl), sh))
-        ev[1].record(s)
-        check(L.ndx_wah_sort(_ptr(keys), n, 0, _ptr(b.ctl), _ptr(b.pairs), _ptr(b.sort_scr), ep, sh))
-        ev[2].record(s)
-        check(L.ndx_wah_emit(_ptr(b.pairs), n, _ptr(b.ctl), _ptr(b.words), _ptr(b.vstart), _ptr(b.values),
-                             _ptr(b.emit_scr), ep, sh))
-        ev[3].record(s)
-        check(L.ndx_wah_table(_ptr(b.values), _ptr(b.vstart), n, _ptr(b.ctl), _ptr(b.entries), sh))
-        ev[4].record(s)
+        for i, (_, call) in enumerate(calls):
+            call()
+            ev[i + 1].record(s)
         torch.cuda.synchronize()
         if rep >= 3:
             times.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
