@@ -1,0 +1,333 @@
+"""bench.py -- WAH index build throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3], the north-star size): per GPU 2^28 uint32
+values, Zipf(s=1) over 65,536 keys, generated with the reference's own
+libstdc++ distributions (mt19937_64(42 + rank)).  A "step" is one full index
+build (plan -> sort -> emit -> table) over that column.
+
+  value  whole-job values/s with the keys already resident in HBM, device
+         time from CUDA events on the launch stream, max over ranks.
+  e2e    the same metric through the public host API per step: pinned keys
+         H2D, the four stages, counts + words + table D2H.
+  roofline  the dominant stage's algorithmic bytes / its live event time,
+         against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the reference's reference_index (1 thread, oracle/_ref) on a
+         bounded sample of the same stream, rank 0 at N=1.
+
+--impl reference runs the reference's own data-parallel CPU build
+(wah::build_index on its simulated device, all host threads) on a bounded
+sample per step (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "WAH index build values/sec"
+UNIT = "values/s"
+
+CONFIGS = {
+    "C4": dict(desc="WAH index build, 2^28 uint32 values per GPU, Zipf(s=1) over 65536 keys",
+               n=1 << 28, kind="zipf", k=65536, seed=42),
+    "C3": dict(desc="WAH index build, 2^26 uint32 values per GPU, 1024 uniform keys (4-stage chain)",
+               n=1 << 26, kind="uniform", k=1024, seed=1),
+    "C5": dict(desc="WAH index build, 2^30 uint32 values, 65536 uniform keys",
+               n=1 << 30, kind="uniform", k=65536, seed=1),
+}
+
+
+def gen_values(cfg, n, rank, out=None):
+    from paper_1709_07781_b200 import gen
+
+    if cfg["kind"] == "zipf":
+        return gen.zipf(cfg["seed"] + rank, n, cfg["k"], 1.0, out)
+    return gen.uniform(cfg["seed"] + rank, n, cfg["k"], out)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the
+    timed region (nvidia-smi -lms in the background)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first sample land before the timed region
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = [[x.strip() for x in ln.split(",")] for ln in out.strip().splitlines() if ln.strip()]
+        sm = [float(r[0]) for r in rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        busy = [s for s in sm if s > 0.5 * (max(mx) if mx else 0)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and
+                          r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return world, rank, local
+
+
+def cpu_baseline(cfg):
+    """reference_index (the reference's CPU path, 1 thread) on a bounded sample."""
+    import oracle
+
+    n = 1 << 25
+    v = gen_values(cfg, n, 0)
+    if oracle.Reference.available():
+        impl, kind = oracle.Reference(), "reference"
+    else:
+        impl, kind = oracle.Port(), "port"
+    t0 = time.perf_counter()
+    impl.digest_of(v)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"wah::reference_index, 1 thread, first 2^25 values of the same stream "
+                      f"({dt:.1f} s)"}
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return 0
+    import oracle
+
+    n = args.ref_sample
+    v = gen_values(cfg, n, 0)
+    cores = os.cpu_count() or 1
+    if oracle.Reference.available():
+        build = lambda: oracle.Reference().build_index_sim(v, cores, 8)  # noqa: E731
+        kind = "reference"
+        what = f"wah::build_index on the reference's simulated device, {cores} compute units, 8-bit digits"
+    else:
+        build = lambda: oracle.Port().reference_index(v)  # noqa: E731
+        kind = "port"
+        what = "C restatement of wah::reference_index, 1 thread"
+        cores = 1
+    for _ in range(args.warmup):
+        build()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        build()
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = n / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "sample_values_per_step": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{what}; {n} values of the same stream per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, cfg):
+    import torch
+
+    from paper_1709_07781_b200 import ndx
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.n or cfg["n"]
+
+    host_keys = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    gen_values(cfg, n, rank, host_keys.numpy().view(np.uint32))
+    keys = host_keys.to(dev)
+    b = ndx.WahBuilder(n, device=local)
+    stream = torch.cuda.current_stream()
+    calls = b.stage_calls(keys, n, row_base=0, stream=stream)
+
+    def sync_all():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        for _, c in calls:
+            c()
+    sync_all()
+
+    # ---- device-resident timed region (inputs 1 GiB/GPU > 126 MB L2)
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(K)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    sync_all()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(K):
+        ev[k][0].record(stream)
+        for i, (_, c) in enumerate(calls):
+            c()
+            ev[k][i + 1].record(stream)
+    t_end.record(stream)
+    sync_all()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end) / K
+    stage_ms = {name: sum(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(K)) / K
+                for i, (name, _) in enumerate(calls)}
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    W, D = b.counts()
+    value = world * n / (ms * 1e-3)
+
+    # ---- end to end through the host API: H2D keys, build, D2H counts+words+table
+    host_words = torch.empty(2 * n, dtype=torch.int32, pin_memory=True)
+    host_ent = torch.empty(3 * n, dtype=torch.int32, pin_memory=True)
+    host_cnt = torch.empty(8, dtype=torch.int32, pin_memory=True)
+    e2e_steps = max(1, min(K, args.e2e_steps))
+    sync_all()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    d2h = 0
+    for _ in range(e2e_steps):
+        keys.copy_(host_keys, non_blocking=True)
+        for _, c in calls:
+            c()
+        host_cnt.copy_(b.ctl[:8], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        cw, cd = host_cnt.numpy().view(np.uint64)[:2]
+        host_words[:int(cw)].copy_(b.words[:int(cw)], non_blocking=True)
+        host_ent[:3 * int(cd)].copy_(b.entries[:3 * int(cd)], non_blocking=True)
+        d2h = 32 + 4 * int(cw) + 12 * int(cd)
+    e1.record(stream)
+    sync_all()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    # ---- roofline of the dominant stage (algorithmic bytes)
+    peak, peak_kind = measured_peaks()
+    passes = 2 if cfg["kind"] == "zipf" or cfg["k"] > 2048 else 1
+    alg = {
+        "plan": 4 * n,
+        "sort": (12 * n + 16 * n * (passes - 1)),
+        "emit": 8 * n + 4 * W + 8 * D,
+        "table": 20 * D,
+    }
+    dom = max(stage_ms, key=stage_ms.get)
+    achieved = alg[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(args.config, {}).get(dom)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "values_per_gpu": n, "keys": cfg["k"],
+                   "distribution": "zipf s=1" if cfg["kind"] == "zipf" else "uniform",
+                   "l2": "inputs larger than L2 (keys 4 B x values per GPU)",
+                   "parallelism": f"row shards x{world}", "words": W, "distinct": D},
+        "stage_ms": stage_ms,
+        "roofline": {"bound": "hbm", "kernel_stage": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes": alg[dom]},
+        "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": 11 * K,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
+    ap.add_argument("--n", type=int, default=0, help="values per GPU (default: the config's)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
