@@ -2,11 +2,11 @@
  * ndactor_c.h -- C ABI of the C++ host runtime (libndactor.so).
  *
  * The C++ API (include/ndactor/*.hpp) is the reference's own surface
- * (p/core/include/ndactor/*.hpp); these extern "C" entry points expose the
- * same operations to non-C++ callers (ctypes / cgo / JNI stubs in
- * INTEGRATION.md) with plain pointers and sizes.  Return 0 on success,
- * otherwise an error code; ndactor_last_error() describes the last failure
- * on the calling thread.
+ * (p/core/include/ndactor/*.hpp).  These extern "C" entry points expose the
+ * same operations to non-C++ callers (the ctypes/cgo/JNI stubs of
+ * INTEGRATION.md) with plain pointers and sizes.  Every function returns 0
+ * on success or a nonzero code; ndactor_last_error() describes the last
+ * failure on the calling thread.  Nothing throws across this boundary.
  */
 #ifndef NDACTOR_C_H
 #define NDACTOR_C_H
@@ -17,6 +17,46 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+/* A runtime = one ActorSystem + one Device (CUDA ordinal) + the four build
+ * stage actors (plan, sort, emit, table) chained table*emit*sort*plan. */
+typedef struct ndactor_runtime ndactor_runtime;
+
+int ndactor_runtime_create(int device_ordinal, unsigned workers, ndactor_runtime** out);
+void ndactor_runtime_destroy(ndactor_runtime* rt);
+const char* ndactor_last_error(void);
+/* The runtime device's in-order stream (cudaStream_t), for callers that
+ * time or order their own work against it. */
+void* ndactor_runtime_stream(ndactor_runtime* rt);
+int ndactor_runtime_synchronize(ndactor_runtime* rt);
+
+/* wah::build_index (p/core/src/wah_builder.cpp:38-307) through the actor
+ * chain: host values in, host index out.  `words`/`entries` are caller
+ * buffers (pinned host memory is fastest) of at least 2n and 3n u32; the
+ * entries are (value, offset, length) triples.  Bit-exact with the
+ * reference's reference_index.  row_base offsets the row ids (shards). */
+int ndactor_wah_build_index(ndactor_runtime* rt, const uint32_t* values, uint64_t n,
+                            uint32_t row_base, uint32_t* words, uint64_t words_cap,
+                            uint32_t* entries, uint64_t entries_cap,
+                            uint64_t* n_words, uint64_t* n_entries);
+
+/* The same chain on keys already resident on the device (d_keys: n u32, not
+ * modified; row ids start at row_base).  The result stays on the device:
+ * *d_counts points at an ndx_wah_counts {words, distinct, min, max},
+ * *d_words at the words, *d_entries at the (value, offset, length) triples.
+ * The pointers stay valid until the next call on this runtime.  Returns as
+ * soon as the work is enqueued on ndactor_runtime_stream (no host sync). */
+int ndactor_wah_build_index_device(ndactor_runtime* rt, const uint32_t* d_keys, uint64_t n,
+                                   uint32_t row_base, uint32_t** d_words, uint32_t** d_entries,
+                                   void** d_counts);
+
+/* BASELINE config 2: `iters` one-warp kernels issued (a) raw, back to back
+ * with the C ABI on the runtime stream, (b) as compute-actor requests where
+ * each request is issued from the previous reply (in_out reference, replies
+ * leave before the kernel runs).  Both end with one synchronisation; host
+ * wall time in milliseconds.  `check` receives the final counter (2*iters). */
+int ndactor_dispatch_probe(ndactor_runtime* rt, uint64_t iters, double* raw_ms, double* actor_ms,
+                           uint64_t* check);
 
 /* Synthetic columns, bit-identical to the reference's generators:
  * std::mt19937(seed) + uniform_int_distribution<u32>(0, cardinality-1)
@@ -29,6 +69,10 @@ void ndactor_gen_zipf(uint64_t seed, uint64_t n, uint32_t k, double s, uint32_t*
 void ndactor_gen_instances(uint32_t seed, uint32_t count, const uint32_t* cards,
                            uint32_t ncards, uint32_t max_rows, uint64_t* sizes,
                            uint32_t* out);
+
+/* "WAH1" index file (p/core/src/wah_index_io.cpp:30-87). */
+int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_t* entries,
+                             uint64_t n_entries, const uint32_t* words, uint64_t n_words);
 
 #ifdef __cplusplus
 }

@@ -65,15 +65,22 @@ def build_ndactor(force: bool = False) -> str:
 
 
 def build_cpp_tests(force: bool = False) -> str | None:
-    srcs = sorted(glob.glob(os.path.join(ROOT, "tests", "cpp", "*.cpp")))
+    """C++ contract tests (tests/cpp): CPU cases need no GPU; GPU cases use
+    real CUDA test kernels and check results against the oracle library."""
+    srcs = sorted(glob.glob(os.path.join(ROOT, "tests", "cpp", "*.cpp")) +
+                  glob.glob(os.path.join(ROOT, "tests", "cpp", "*.cu")))
     if not srcs:
         return None
     out = os.path.join(LIB, "ndactor_tests")
+    oracle_dir = os.path.join(ROOT, "oracle", "_build")
+    if not os.path.exists(os.path.join(oracle_dir, "libwah_oracle.so")):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), os.path.join("_build", "libwah_oracle.so")],
+                       check=True)
     deps = srcs + glob.glob(os.path.join(ROOT, "tests", "cpp", "*.hpp")) + [os.path.join(LIB, "libndactor.so")]
     if force or _stale(out, deps):
-        cxx = os.environ.get("CXX", "g++")
-        _run([cxx, "-std=c++20", "-O1", "-g", "-pthread", "-I" + INC, "-o", out, *srcs,
-              "-L" + LIB, "-lndactor", "-lndx", "-Wl,-rpath," + LIB])
+        _run([NVCC, *ARCH, "-O1", "-g", "-std=c++20", "-Xcompiler", "-pthread", "-I" + INC,
+              "-o", out, *srcs, "-L" + LIB, "-lndactor", "-lndx", "-L" + oracle_dir, "-lwah_oracle",
+              "-Xlinker", "-rpath," + LIB + ":" + oracle_dir, "-cudart", "static"])
     return out
 
 

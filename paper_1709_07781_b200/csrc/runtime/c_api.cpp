@@ -1,0 +1,228 @@
+// extern "C" surface of the runtime (include/ndactor_c.h).
+#include "ndactor_c.h"
+
+#include <chrono>
+#include <cstring>
+#include <future>
+#include <string>
+
+#include "ndactor/compute_actor.hpp"
+#include "ndactor/wah_device.hpp"
+#include "ndactor/wah_io.hpp"
+#include "ndx.h"
+
+using namespace ndactor;
+
+struct ndactor_runtime {
+  std::unique_ptr<Device> dev;
+  std::unique_ptr<ActorSystem> sys;
+  wah::IndexStages stages;
+  wah::IndexStages shard;  // stages for a nonzero row base (multi-GPU shards)
+  std::uint32_t shard_base = 0;
+  wah::DeviceIndex last;   // result of the last device build (kept alive)
+  ActorHandle probe;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  } catch (...) {
+    g_err = "unknown error";
+  }
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ndactor_last_error(void) { return g_err.c_str(); }
+
+int ndactor_runtime_create(int device_ordinal, unsigned workers, ndactor_runtime** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null out pointer");
+    auto rt = std::make_unique<ndactor_runtime>();
+    DeviceConfig cfg;
+    cfg.ordinal = device_ordinal;
+    rt->dev = std::make_unique<Device>(cfg);
+    rt->sys = std::make_unique<ActorSystem>(workers ? workers : 2u);
+    rt->stages = wah::spawn_index_stages(*rt->sys, *rt->dev);
+    *out = rt.release();
+    return 0;
+  });
+}
+
+void ndactor_runtime_destroy(ndactor_runtime* rt) {
+  if (!rt) return;
+  try {
+    rt->last = wah::DeviceIndex{};
+    rt->sys->await_idle();
+    rt->dev->await_all();
+    rt->sys->shutdown();
+  } catch (...) {
+  }
+  delete rt;
+}
+
+void* ndactor_runtime_stream(ndactor_runtime* rt) { return rt ? rt->dev->stream() : nullptr; }
+
+int ndactor_runtime_synchronize(ndactor_runtime* rt) {
+  return guarded([&] {
+    rt->dev->await_all();
+    return 0;
+  });
+}
+
+int ndactor_wah_build_index(ndactor_runtime* rt, const uint32_t* values, uint64_t n,
+                            uint32_t row_base, uint32_t* words, uint64_t words_cap,
+                            uint32_t* entries, uint64_t entries_cap, uint64_t* n_words,
+                            uint64_t* n_entries) {
+  return guarded([&] {
+    if (!rt) throw std::invalid_argument("null runtime");
+    if (n_words) *n_words = 0;
+    if (n_entries) *n_entries = 0;
+    if (n == 0) return 0;
+    if (row_base != 0) throw std::invalid_argument("row_base needs ndactor_wah_build_index_device");
+    Device& dev = *rt->dev;
+    Buffer keys = dev.create_buffer_uninit(ElemType::u32, std::int64_t(n));
+    Event wrote = dev.enqueue_native(
+        "h2d_keys", [&](void* s) { return ndx_memcpy_h2d_async(keys.data(), values, n * 4, s); }, {});
+    wah::DeviceIndex d = wah::build_index_device(*rt->sys, rt->stages, MemRef(keys, wrote), std::uint32_t(n));
+    // counts, then exactly W words and D entries straight into the caller's buffers
+    ndx_wah_counts c{};
+    std::vector<Event> deps{d.entries.pending()};
+    Event got = dev.enqueue_native(
+        "d2h_counts", [&](void* s) { return ndx_memcpy_d2h_async(&c, d.cfg.buffer().data(), sizeof c, s); },
+        deps);
+    if (got.await() == EventState::failed) throw std::runtime_error(got.error());
+    if (c.words > words_cap || 3 * c.distinct > entries_cap) throw std::length_error("output buffers too small");
+    Event rd = dev.enqueue_native(
+        "d2h_index",
+        [&](void* s) -> int {
+          int rc = ndx_memcpy_d2h_async(words, d.words.buffer().data(), c.words * 4, s);
+          if (!rc) rc = ndx_memcpy_d2h_async(entries, d.entries.buffer().data(), c.distinct * 12, s);
+          return rc;
+        },
+        {});
+    if (rd.await() == EventState::failed) throw std::runtime_error(rd.error());
+    release(d.cfg);
+    release(d.words);
+    release(d.entries);
+    if (n_words) *n_words = c.words;
+    if (n_entries) *n_entries = c.distinct;
+    return 0;
+  });
+}
+
+int ndactor_wah_build_index_device(ndactor_runtime* rt, const uint32_t* d_keys, uint64_t n,
+                                   uint32_t row_base, uint32_t** d_words, uint32_t** d_entries,
+                                   void** d_counts) {
+  return guarded([&] {
+    if (!rt) throw std::invalid_argument("null runtime");
+    rt->last = wah::DeviceIndex{};  // previous result: released in stream order
+    if (n == 0) return 0;
+    Device& dev = *rt->dev;
+    wah::IndexStages* st = &rt->stages;
+    if (row_base != 0) {
+      if (!rt->shard.chain.valid() || rt->shard_base != row_base) {
+        if (rt->shard.chain.valid())
+          for (const ActorHandle& a : {rt->shard.chain, rt->shard.table, rt->shard.emit, rt->shard.sort,
+                                       rt->shard.plan})
+            rt->sys->terminate(a);
+        rt->shard = wah::spawn_index_stages(*rt->sys, dev, row_base);
+        rt->shard_base = row_base;
+      }
+      st = &rt->shard;
+    }
+    Buffer keys = dev.wrap_buffer(const_cast<uint32_t*>(d_keys), ElemType::u32, std::int64_t(n),
+                                  Access::read_only);
+    rt->last = wah::build_index_device(*rt->sys, *st, MemRef(keys, Event{}), std::uint32_t(n));
+    if (d_words) *d_words = static_cast<uint32_t*>(rt->last.words.buffer().data());
+    if (d_entries) *d_entries = static_cast<uint32_t*>(rt->last.entries.buffer().data());
+    if (d_counts) *d_counts = rt->last.cfg.buffer().data();
+    return 0;
+  });
+}
+
+int ndactor_dispatch_probe(ndactor_runtime* rt, uint64_t iters, double* raw_ms, double* actor_ms,
+                           uint64_t* check) {
+  return guarded([&] {
+    Device& dev = *rt->dev;
+    ActorSystem& sys = *rt->sys;
+    using clk = std::chrono::steady_clock;
+    Buffer counter = dev.create_buffer(ElemType::u32, 1);
+    dev.await_all();
+
+    // (a) raw: back-to-back launches on the runtime stream, one sync
+    auto t0 = clk::now();
+    for (uint64_t i = 0; i < iters; ++i) {
+      int rc = ndx_tiny_increment(static_cast<uint32_t*>(counter.data()), dev.stream());
+      if (rc) throw std::runtime_error(ndx_error_string(rc));
+    }
+    ndx_stream_synchronize(dev.stream());
+    *raw_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+
+    // (b) actor: each request issued from the previous reply
+    if (!rt->probe.valid()) {
+      ComputeActorSpec spec;
+      spec.kernel = KernelDef("tiny_increment", [](const LaunchParams& lp) -> int {
+        return ndx_tiny_increment(static_cast<uint32_t*>(lp.ptr[0]), lp.stream);
+      });
+      spec.range = NdRange::linear(32, 32);
+      spec.args = {ArgSpec::in_out(ElemType::u32, ArgMode::ref, ArgMode::ref)};
+      rt->probe = spawn_compute(sys, dev, std::move(spec));
+    }
+    ActorHandle actor = rt->probe;
+    auto done = std::make_shared<std::promise<Reply>>();
+    auto fut = done->get_future();
+    struct Loop {
+      ActorSystem* sys;
+      ActorHandle actor;
+      uint64_t left;
+      std::shared_ptr<std::promise<Reply>> done;
+    };
+    auto loop = std::make_shared<Loop>(Loop{&sys, actor, iters, done});
+    std::function<void(Reply)> step;
+    auto stepp = std::make_shared<std::function<void(Reply)>>();
+    *stepp = [loop, stepp](Reply r) {
+      if (is_error(r) || --loop->left == 0) {
+        loop->done->set_value(std::move(r));
+        return;
+      }
+      loop->sys->request(loop->actor, std::move(std::get<Message>(r))).then(*stepp);
+    };
+    MemRef ref(counter, Event{});
+    auto t1 = clk::now();
+    sys.request(actor, Message::of(ref)).then(*stepp);
+    Reply last = fut.get();
+    if (is_error(last)) throw std::runtime_error(get_error(last).what);
+    std::vector<uint32_t> v = retrieve_u32(get_message(last).at(0).as_ref());
+    *actor_ms = std::chrono::duration<double, std::milli>(clk::now() - t1).count();
+    *stepp = nullptr;  // break the self-reference
+    if (check) *check = v.empty() ? 0 : v[0];
+    return 0;
+  });
+}
+
+int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_t* entries,
+                             uint64_t n_entries, const uint32_t* words, uint64_t n_words) {
+  return guarded([&] {
+    wah::WahIndex idx;
+    idx.row_count = row_count;
+    idx.entries.resize(n_entries);
+    for (uint64_t i = 0; i < n_entries; ++i)
+      idx.entries[i] = wah::IndexEntry{entries[3 * i], entries[3 * i + 1], entries[3 * i + 2]};
+    idx.words.assign(words, words + n_words);
+    wah::write_index_file(path, idx);
+    return 0;
+  });
+}
+
+}  // extern "C"

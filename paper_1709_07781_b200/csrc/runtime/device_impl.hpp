@@ -1,0 +1,94 @@
+// Internal: the CUDA device behind ndactor::Device and the Event state.
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ndactor/device.hpp"
+#include "ndactor/event.hpp"
+
+namespace ndactor {
+
+struct Event::State {
+  std::uint64_t id = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  EventState st = EventState::pending;
+  std::string error;
+  std::vector<Callback> callbacks;
+  Clock::time_point enqueue_tp = Clock::now();
+  Clock::time_point exec_start_tp{};
+  Clock::time_point terminal_tp{};
+  std::atomic<bool> exec_started{false};
+  // device binding: the stream position (0 = not issued on a device yet)
+  std::weak_ptr<detail::DeviceImpl> dev;
+  std::atomic<std::uint64_t> seq{0};
+  bool awaited = false;  // someone blocks in await() (guarded by mu)
+  // runs on the completing thread right before the terminal transition
+  std::function<void()> before_complete;
+};
+
+namespace detail {
+
+struct DeviceImpl : std::enable_shared_from_this<DeviceImpl> {
+  int ordinal = 0;
+  void* stream = nullptr;
+  std::size_t max_group = 1024;
+
+  // issue order == stream order == sequence order
+  std::mutex issue_mu;
+  std::uint64_t issued = 0;
+  bool broken = false;
+  std::string broken_why;
+
+  // completion tracking
+  std::mutex watch_mu;
+  std::condition_variable watch_cv;
+  std::multimap<std::uint64_t, std::shared_ptr<Event::State>> watched;
+  std::atomic<std::uint64_t> completed{0};
+  bool stopping = false;
+  std::thread completer;
+
+  // commands waiting on host events / unissued dependencies
+  std::mutex defer_mu;
+  std::condition_variable defer_cv;
+  std::size_t deferred = 0;
+
+  std::atomic<std::size_t> live{0};
+  std::atomic<std::uint64_t> next_buffer_id{1};
+
+  // pinned staging blocks for asynchronous reads, by power-of-two size
+  std::mutex pin_mu;
+  std::multimap<std::size_t, void*> pinned_free;
+
+  void start();
+  void stop();
+  /// Completes every watched event with seq <= s (runs callbacks).
+  void complete_upto(std::uint64_t s);
+  void fail_all(const std::string& why);
+  /// Blocks until everything issued so far is done; returns false on a
+  /// sticky device error (then every pending event has been failed).
+  bool sync_now();
+  /// Non-blocking progress check used by Event::state().
+  void poll();
+  void watch(const std::shared_ptr<Event::State>& st);
+  void completer_loop();
+
+  void* pinned_get(std::size_t bytes, std::size_t& cap);
+  void pinned_put(void* p, std::size_t cap);
+};
+
+Event make_device_event(const std::shared_ptr<DeviceImpl>& d);
+void finish_event(const std::shared_ptr<Event::State>& st, bool ok, std::string why);
+
+}  // namespace detail
+}  // namespace ndactor

@@ -1,0 +1,112 @@
+"""ctypes binding of the C++ runtime's C ABI (include/ndactor_c.h).
+
+`Runtime` owns one ActorSystem + Device + the four build-stage compute actors
+(libndactor.so).  `build_index` is the public host call (host values in, host
+index out, through the actor chain); `build_index_device` runs the chain on
+device-resident keys and leaves the index in HBM."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+_LIB = None
+_vp = ctypes.c_void_p
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_u64 = ctypes.c_uint64
+
+
+class RuntimeError_(RuntimeError):
+    pass
+
+
+def lib_path() -> str:
+    return os.path.join(_build.LIB, "libndactor.so")
+
+
+def load() -> ctypes.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(lib_path()):
+            _build.build_all()
+        lib = ctypes.CDLL(lib_path())
+        sig = {
+            "ndactor_runtime_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint, ctypes.POINTER(_vp)]),
+            "ndactor_runtime_destroy": (None, [_vp]),
+            "ndactor_last_error": (ctypes.c_char_p, []),
+            "ndactor_runtime_stream": (_vp, [_vp]),
+            "ndactor_runtime_synchronize": (ctypes.c_int, [_vp]),
+            "ndactor_wah_build_index": (ctypes.c_int, [_vp, _vp, _u64, ctypes.c_uint32, _vp, _u64, _vp, _u64,
+                                                       ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+            "ndactor_wah_build_index_device": (ctypes.c_int, [_vp, _vp, _u64, ctypes.c_uint32, ctypes.POINTER(_vp),
+                                                              ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+            "ndactor_dispatch_probe": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(ctypes.c_double),
+                                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
+            "ndactor_write_index_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, _vp, _u64, _vp, _u64]),
+        }
+        for name, (rt, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = rt
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise RuntimeError_(f"{what}: {load().ndactor_last_error().decode()}")
+
+
+class Runtime:
+    def __init__(self, device: int = 0, workers: int = 2):
+        self.lib = load()
+        h = _vp()
+        _check(self.lib.ndactor_runtime_create(device, workers, ctypes.byref(h)), "runtime_create")
+        self.h = h
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.ndactor_runtime_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.ndactor_runtime_stream(self.h) or 0)
+
+    def synchronize(self) -> None:
+        _check(self.lib.ndactor_runtime_synchronize(self.h), "synchronize")
+
+    def build_index(self, values: np.ndarray, words_out=None, entries_out=None):
+        """wah::build_index: host values in, (row_count, entries (D,3), words) out."""
+        v = np.ascontiguousarray(values, dtype=np.uint32)
+        n = v.size
+        words = words_out if words_out is not None else np.empty(max(2 * n, 1), np.uint32)
+        ent = entries_out if entries_out is not None else np.empty(max(3 * n, 1), np.uint32)
+        nw, ne = _u64(), _u64()
+        _check(self.lib.ndactor_wah_build_index(self.h, v.ctypes.data if n else None, n, 0, words.ctypes.data,
+                                                words.size, ent.ctypes.data, ent.size, ctypes.byref(nw),
+                                                ctypes.byref(ne)), "build_index")
+        return n, ent[: 3 * ne.value].reshape(-1, 3), words[: nw.value]
+
+    def build_index_device(self, d_keys: int, n: int, row_base: int = 0):
+        """Enqueue the chain on device keys; returns device pointers
+        (counts, words, entries), valid until the next call."""
+        w, e, c = _vp(), _vp(), _vp()
+        _check(self.lib.ndactor_wah_build_index_device(self.h, d_keys, n, row_base, ctypes.byref(w),
+                                                       ctypes.byref(e), ctypes.byref(c)), "build_index_device")
+        return c.value, w.value, e.value
+
+    def dispatch_probe(self, iters: int = 10000):
+        raw, act, chk = ctypes.c_double(), ctypes.c_double(), _u64()
+        _check(self.lib.ndactor_dispatch_probe(self.h, iters, ctypes.byref(raw), ctypes.byref(act),
+                                               ctypes.byref(chk)), "dispatch_probe")
+        return raw.value, act.value, chk.value
