@@ -57,6 +57,7 @@ struct KernelArg {
 /// shared-memory block (`smem_offset[i]`, `len[i]` elements); scalar args
 /// are in `scalar[i]`.
 struct LaunchParams {
+  static constexpr std::size_t kMaxArgs = 16;
   void* stream = nullptr;  // cudaStream_t
   unsigned rank = 1;
   std::array<unsigned, 3> grid{1, 1, 1};
@@ -64,10 +65,11 @@ struct LaunchParams {
   std::array<std::size_t, 3> offset{0, 0, 0};
   std::array<std::size_t, 3> global{1, 1, 1};
   std::size_t shared_bytes = 0;
-  std::vector<void*> ptr;
-  std::vector<std::size_t> len;
-  std::vector<std::size_t> smem_offset;
-  std::vector<Scalar> scalar;
+  std::size_t nargs = 0;
+  std::array<void*, kMaxArgs> ptr{};
+  std::array<std::size_t, kMaxArgs> len{};
+  std::array<std::size_t, kMaxArgs> smem_offset{};
+  std::array<Scalar, kMaxArgs> scalar{};
 };
 
 /// Returns 0 or a CUDA/ndx error code; must not throw.

@@ -57,6 +57,10 @@ int ndactor_wah_build_index_device(ndactor_runtime* rt, const uint32_t* d_keys, 
  * wall time in milliseconds.  `check` receives the final counter (2*iters). */
 int ndactor_dispatch_probe(ndactor_runtime* rt, uint64_t iters, double* raw_ms, double* actor_ms,
                            uint64_t* check);
+/* Same, with the breakdown: out[0] raw total ms, out[1] raw host enqueue ms,
+ * out[2] actor total ms, out[3] actor chain with a no-op launcher (pure host
+ * cost of `iters` hops), out[4] final counter value. */
+int ndactor_dispatch_probe_ex(ndactor_runtime* rt, uint64_t iters, double* out);
 
 /* Synthetic columns, bit-identical to the reference's generators:
  * std::mt19937(seed) + uniform_int_distribution<u32>(0, cardinality-1)

@@ -151,12 +151,58 @@ int ndactor_wah_build_index_device(ndactor_runtime* rt, const uint32_t* d_keys, 
   });
 }
 
-int ndactor_dispatch_probe(ndactor_runtime* rt, uint64_t iters, double* raw_ms, double* actor_ms,
-                           uint64_t* check) {
+namespace {
+
+// Chain `iters` requests through `actor`, each issued from the previous
+// reply; returns the last reply.
+Reply chain_requests(ActorSystem& sys, ActorHandle actor, Message first, uint64_t iters) {
+  struct Loop {
+    ActorSystem* sys;
+    ActorHandle actor;
+    uint64_t left;
+    std::promise<Reply> done;
+    std::function<void(Reply)> step;
+  };
+  auto loop = std::make_shared<Loop>();
+  loop->sys = &sys;
+  loop->actor = actor;
+  loop->left = iters;
+  Loop* lp = loop.get();
+  loop->step = [lp](Reply r) {
+    if (is_error(r) || --lp->left == 0) {
+      lp->done.set_value(std::move(r));
+      return;
+    }
+    lp->sys->request(lp->actor, std::move(std::get<Message>(r))).then(std::ref(lp->step));
+  };
+  auto fut = loop->done.get_future();
+  sys.request(actor, std::move(first)).then(std::ref(loop->step));
+  Reply last = fut.get();
+  sys.await_idle();
+  return last;
+}
+
+ActorHandle tiny_actor(ActorSystem& sys, Device& dev, bool launch) {
+  ComputeActorSpec spec;
+  if (launch)
+    spec.kernel = KernelDef("tiny_increment", [](const LaunchParams& lp) -> int {
+      return ndx_tiny_increment(static_cast<uint32_t*>(lp.ptr[0]), lp.stream);
+    });
+  else
+    spec.kernel = KernelDef("host_only", [](const LaunchParams&) -> int { return 0; });
+  spec.range = NdRange::linear(32, 32);
+  spec.args = {ArgSpec::in_out(ElemType::u32, ArgMode::ref, ArgMode::ref)};
+  return spawn_compute(sys, dev, std::move(spec));
+}
+
+}  // namespace
+
+int ndactor_dispatch_probe_ex(ndactor_runtime* rt, uint64_t iters, double* out /* [5] */) {
   return guarded([&] {
     Device& dev = *rt->dev;
     ActorSystem& sys = *rt->sys;
     using clk = std::chrono::steady_clock;
+    auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
     Buffer counter = dev.create_buffer(ElemType::u32, 1);
     dev.await_all();
 
@@ -166,49 +212,39 @@ int ndactor_dispatch_probe(ndactor_runtime* rt, uint64_t iters, double* raw_ms, 
       int rc = ndx_tiny_increment(static_cast<uint32_t*>(counter.data()), dev.stream());
       if (rc) throw std::runtime_error(ndx_error_string(rc));
     }
+    out[1] = ms_since(t0);  // host enqueue time alone
     ndx_stream_synchronize(dev.stream());
-    *raw_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    out[0] = ms_since(t0);
 
-    // (b) actor: each request issued from the previous reply
-    if (!rt->probe.valid()) {
-      ComputeActorSpec spec;
-      spec.kernel = KernelDef("tiny_increment", [](const LaunchParams& lp) -> int {
-        return ndx_tiny_increment(static_cast<uint32_t*>(lp.ptr[0]), lp.stream);
-      });
-      spec.range = NdRange::linear(32, 32);
-      spec.args = {ArgSpec::in_out(ElemType::u32, ArgMode::ref, ArgMode::ref)};
-      rt->probe = spawn_compute(sys, dev, std::move(spec));
-    }
-    ActorHandle actor = rt->probe;
-    auto done = std::make_shared<std::promise<Reply>>();
-    auto fut = done->get_future();
-    struct Loop {
-      ActorSystem* sys;
-      ActorHandle actor;
-      uint64_t left;
-      std::shared_ptr<std::promise<Reply>> done;
-    };
-    auto loop = std::make_shared<Loop>(Loop{&sys, actor, iters, done});
-    std::function<void(Reply)> step;
-    auto stepp = std::make_shared<std::function<void(Reply)>>();
-    *stepp = [loop, stepp](Reply r) {
-      if (is_error(r) || --loop->left == 0) {
-        loop->done->set_value(std::move(r));
-        return;
-      }
-      loop->sys->request(loop->actor, std::move(std::get<Message>(r))).then(*stepp);
-    };
+    // (b) through a compute actor, each request issued from the previous reply
+    if (!rt->probe.valid()) rt->probe = tiny_actor(sys, dev, true);
     MemRef ref(counter, Event{});
     auto t1 = clk::now();
-    sys.request(actor, Message::of(ref)).then(*stepp);
-    Reply last = fut.get();
+    Reply last = chain_requests(sys, rt->probe, Message::of(ref), iters);
     if (is_error(last)) throw std::runtime_error(get_error(last).what);
     std::vector<uint32_t> v = retrieve_u32(get_message(last).at(0).as_ref());
-    *actor_ms = std::chrono::duration<double, std::milli>(clk::now() - t1).count();
-    *stepp = nullptr;  // break the self-reference
-    if (check) *check = v.empty() ? 0 : v[0];
+    out[2] = ms_since(t1);
+    out[4] = v.empty() ? 0 : double(v[0]);
+
+    // (c) the same chain with a launcher that issues nothing: host cost of a hop
+    ActorHandle host_only = tiny_actor(sys, dev, false);
+    auto t2 = clk::now();
+    Reply l2 = chain_requests(sys, host_only, Message::of(get_message(last).at(0).as_ref()), iters);
+    out[3] = ms_since(t2);
+    sys.terminate(host_only);
     return 0;
   });
+}
+
+int ndactor_dispatch_probe(ndactor_runtime* rt, uint64_t iters, double* raw_ms, double* actor_ms,
+                           uint64_t* check) {
+  double r[5] = {};
+  int rc = ndactor_dispatch_probe_ex(rt, iters, r);
+  if (rc) return rc;
+  *raw_ms = r[0];
+  *actor_ms = r[2];
+  if (check) *check = uint64_t(r[4]);
+  return 0;
 }
 
 int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_t* entries,

@@ -157,6 +157,40 @@ void* DeviceImpl::pinned_get(std::size_t bytes, std::size_t& cap) {
   return p;
 }
 
+std::size_t DeviceImpl::size_class(std::size_t bytes) {
+  // 1/8-octave classes: at most 12.5% slack, few distinct classes
+  if (bytes <= 4096) return 4096;
+  std::size_t p = std::size_t(1) << (63 - __builtin_clzll(bytes - 1));  // <= bytes-1
+  const std::size_t step = p / 8;
+  return (bytes + step - 1) / step * step;
+}
+
+void* DeviceImpl::block_get(std::size_t cls) {
+  auto it = block_cache.find(cls);
+  if (it == block_cache.end()) return nullptr;
+  void* p = it->second;
+  block_cache.erase(it);
+  cached_bytes -= cls;
+  return p;
+}
+
+void DeviceImpl::block_put(void* p, std::size_t cls) {
+  block_cache.emplace(cls, p);
+  cached_bytes += cls;
+  while (cached_bytes > kCacheLimit && !block_cache.empty()) {
+    auto it = std::prev(block_cache.end());  // drop the largest
+    ndx_free_async(it->second, stream);
+    cached_bytes -= it->first;
+    block_cache.erase(it);
+  }
+}
+
+void DeviceImpl::block_trim() {
+  for (auto& kv : block_cache) ndx_free_async(kv.second, stream);
+  block_cache.clear();
+  cached_bytes = 0;
+}
+
 void DeviceImpl::pinned_put(void* p, std::size_t cap) {
   std::lock_guard<std::mutex> l(pin_mu);
   pinned_free.emplace(cap, p);
@@ -299,6 +333,10 @@ Device::~Device() {
   }
   impl_->stop();
   {
+    std::lock_guard<std::mutex> l(impl_->issue_mu);
+    impl_->block_trim();
+  }
+  {
     std::lock_guard<std::mutex> l(impl_->pin_mu);
     for (auto& kv : impl_->pinned_free) ndx_host_free(kv.second);
     impl_->pinned_free.clear();
@@ -320,9 +358,18 @@ Buffer make_buffer(Device* self, const std::shared_ptr<DeviceImpl>& d, ElemType 
   st->access = access;
   st->device = self;
   const std::size_t bytes = std::max<std::size_t>(st->length * elem_size(type), 16);
+  const std::size_t cls = DeviceImpl::size_class(bytes);
   {
     std::lock_guard<std::mutex> l(d->issue_mu);
-    int rc = ndx_malloc_async(&st->ptr, bytes, d->stream);
+    int rc = 0;
+    st->ptr = d->block_get(cls);
+    if (!st->ptr) {
+      rc = ndx_malloc_async(&st->ptr, cls, d->stream);
+      if (rc != 0) {  // out of memory: give the cache back and retry once
+        d->block_trim();
+        rc = ndx_malloc_async(&st->ptr, cls, d->stream);
+      }
+    }
     if (rc == 0 && zero) rc = ndx_memset_async(st->ptr, 0, bytes, d->stream);
     if (rc != 0) throw DeviceError(std::string("device allocation failed: ") + ndx_error_string(rc));
   }
@@ -367,7 +414,8 @@ void Device::free_buffer(const Buffer& b) {
   // `freed` and fail instead of touching released memory.
   if (!b.state().owned) return;
   std::lock_guard<std::mutex> l(impl_->issue_mu);
-  ndx_free_async(b.state().ptr, impl_->stream);
+  const std::size_t bytes = std::max<std::size_t>(b.bytes(), 16);
+  impl_->block_put(b.state().ptr, DeviceImpl::size_class(bytes));
 }
 
 std::size_t Device::live_buffers() const { return impl_->live.load(); }
@@ -422,55 +470,94 @@ Event Device::enqueue_read_bytes(const Buffer& b, std::shared_ptr<std::vector<st
   return ev;
 }
 
-Event Device::enqueue_kernel(KernelDef kernel, NdRange range, std::vector<KernelArg> args,
+Event Device::enqueue_kernel(const KernelDef& kernel, NdRange range, std::vector<KernelArg> args,
                              std::vector<Event> deps) {
   if (!kernel.launch) throw DeviceError("kernel has no launcher");
+  if (args.size() > LaunchParams::kMaxArgs) throw DeviceError("too many kernel arguments");
   check_deps(deps);
   for (const KernelArg& a : args)
     if (a.kind == KernelArg::Kind::global) check_target(this, a.buffer);
   const auto local = resolve_local(range, cfg_.max_group_size);
 
-  auto p = std::make_shared<LaunchParams>();
-  p->rank = range.rank;
-  p->offset = range.offset;
-  p->global = range.global;
+  LaunchParams p;
+  p.rank = range.rank;
+  p.offset = range.offset;
+  p.global = range.global;
   for (int d = 0; d < 3; ++d) {
-    p->block[d] = unsigned(local[d]);
-    p->grid[d] = unsigned(range.global[d] / local[d]);
+    p.block[d] = unsigned(local[d]);
+    p.grid[d] = unsigned(range.global[d] / local[d]);
   }
-  p->ptr.resize(args.size(), nullptr);
-  p->len.resize(args.size(), 0);
-  p->smem_offset.resize(args.size(), 0);
-  p->scalar.resize(args.size());
+  p.nargs = args.size();
   std::size_t smem = 0;
-  std::vector<std::shared_ptr<detail::BufferState>> bufs;
   for (std::size_t i = 0; i < args.size(); ++i) {
     const KernelArg& a = args[i];
     switch (a.kind) {
       case KernelArg::Kind::global:
-        p->ptr[i] = a.buffer.data();
-        p->len[i] = a.buffer.length();
-        bufs.push_back(a.buffer.shared_state());
+        p.ptr[i] = a.buffer.data();
+        p.len[i] = a.buffer.length();
         break;
       case KernelArg::Kind::local:
         smem = (smem + 15) & ~std::size_t(15);
-        p->smem_offset[i] = smem;
-        p->len[i] = a.local_len;
+        p.smem_offset[i] = smem;
+        p.len[i] = a.local_len;
         smem += a.local_len * elem_size(a.local_type);
         break;
       case KernelArg::Kind::scalar:
-        p->scalar[i] = a.value;
+        p.scalar[i] = a.value;
         break;
     }
   }
-  p->shared_bytes = smem;
-  Launcher launch = std::move(kernel.launch);
-  Issue w{kernel.name, [p, launch, bufs](void* s) -> int {
+  p.shared_bytes = smem;
+
+  // Fast path: every dependency is complete or issued earlier on this
+  // device's stream -> launch right here, nothing allocated for the command.
+  bool direct = true;
+  for (const Event& dep : deps) {
+    auto& ds = *dep.shared_state();
+    EventState st;
+    {
+      std::lock_guard<std::mutex> l(ds.mu);
+      st = ds.st;
+    }
+    if (st == EventState::complete) continue;
+    if (st == EventState::failed) {
+      direct = false;
+      break;
+    }
+    auto dd = ds.dev.lock();
+    if (!(dd == impl_ && ds.seq.load(std::memory_order_acquire) != 0)) {
+      direct = false;
+      break;
+    }
+  }
+  if (direct) {
+    Event ev = detail::make_device_event(impl_);
+    std::lock_guard<std::mutex> l(impl_->issue_mu);
+    if (impl_->broken) {
+      detail::finish_event(ev.shared_state(), false, impl_->broken_why);
+      return ev;
+    }
+    ev.mark_exec_start();
+    p.stream = impl_->stream;
+    const int rc = kernel.launch(p);
+    if (rc != 0) {
+      detail::finish_event(ev.shared_state(), false, "kernel " + kernel.name + ": " + ndx_error_string(rc));
+      return ev;
+    }
+    ev.shared_state()->seq.store(++impl_->issued, std::memory_order_release);
+    return ev;
+  }
+
+  std::vector<std::shared_ptr<detail::BufferState>> bufs;
+  for (const KernelArg& a : args)
+    if (a.kind == KernelArg::Kind::global) bufs.push_back(a.buffer.shared_state());
+  auto pp = std::make_shared<LaunchParams>(p);
+  Launcher launch = kernel.launch;
+  Issue w{kernel.name, [pp, launch, bufs](void* s) -> int {
             for (auto& b : bufs)
               if (b->freed.load()) return NDX_E_INVALID;  // freed while deferred
-            LaunchParams& lp = *p;
-            lp.stream = s;
-            return launch(lp);
+            pp->stream = s;
+            return launch(*pp);
           }, {}};
   return submit(impl_, std::move(w), deps);
 }

@@ -70,6 +70,19 @@ struct DeviceImpl : std::enable_shared_from_this<DeviceImpl> {
   std::mutex pin_mu;
   std::multimap<std::size_t, void*> pinned_free;
 
+  // Device blocks released by free_buffer, kept for reuse by size class.
+  // Frees and allocations are both ordered on the one stream, so handing a
+  // released block to the next allocation is safe without any wait -- the
+  // same rule stream-ordered pools follow, minus their per-call cost for
+  // multi-GB blocks.  Guarded by issue_mu.
+  std::multimap<std::size_t, void*> block_cache;
+  std::size_t cached_bytes = 0;
+  static constexpr std::size_t kCacheLimit = std::size_t(64) << 30;
+  static std::size_t size_class(std::size_t bytes);
+  void* block_get(std::size_t cls);
+  void block_put(void* p, std::size_t cls);
+  void block_trim();
+
   void start();
   void stop();
   /// Completes every watched event with seq <= s (runs callbacks).

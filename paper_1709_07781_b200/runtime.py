@@ -45,6 +45,7 @@ def load() -> ctypes.CDLL:
                                                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
             "ndactor_dispatch_probe": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(ctypes.c_double),
                                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
+            "ndactor_dispatch_probe_ex": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(ctypes.c_double)]),
             "ndactor_write_index_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, _vp, _u64, _vp, _u64]),
         }
         for name, (rt, args) in sig.items():
@@ -104,6 +105,12 @@ class Runtime:
         _check(self.lib.ndactor_wah_build_index_device(self.h, d_keys, n, row_base, ctypes.byref(w),
                                                        ctypes.byref(e), ctypes.byref(c)), "build_index_device")
         return c.value, w.value, e.value
+
+    def dispatch_probe_ex(self, iters: int = 10000) -> dict:
+        out = (ctypes.c_double * 5)()
+        _check(self.lib.ndactor_dispatch_probe_ex(self.h, iters, out), "dispatch_probe_ex")
+        return {"raw_ms": out[0], "raw_enqueue_ms": out[1], "actor_ms": out[2], "actor_host_only_ms": out[3],
+                "counter": int(out[4])}
 
     def dispatch_probe(self, iters: int = 10000):
         raw, act, chk = ctypes.c_double(), ctypes.c_double(), _u64()
