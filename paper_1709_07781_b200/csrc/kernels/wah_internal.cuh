@@ -43,6 +43,7 @@ struct Ctl {
   uint32_t zero_end;
   // ---- written by the plan kernel ----
   uint32_t epoch;      // look-back status tag of this build (from the sort scratch counter)
+  uint32_t row_hi;     // largest row id of the build (row_base + n - 1), written by the sort
   SortPlan plan;
 };
 

@@ -495,6 +495,8 @@ __device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint3
 // (P-1-q) is even, so the last pass lands in X.
 template <int MAXB>
 __global__ __launch_bounds__(kSortThreads, 3) void k_pass(SortArgs a, int which) {
+  if (which < 0 && blockIdx.x == 0 && threadIdx.x == 0)
+    a.ctl->row_hi = a.row_base + uint32_t(a.n - 1);  // read by the emit stage
   PassInfo pi;
   if (!pass_info(a, which, pi)) return;
   extern __shared__ __align__(16) unsigned char smem[];

@@ -153,3 +153,32 @@ def test_compaction_drops_zeros_keeps_order(prims, port):  # test_wah_device.cpp
         else:
             x = rng.integers(0, 3, n).astype(np.uint32)
         assert np.array_equal(prims.compact(x), port.filter_nonzero(x)), it
+
+
+def _shift_index(ref, k_chunks: int):
+    """The index of the same values placed at rows 31*k_chunks + i: every
+    value's leading zero-fill grows by k_chunks chunks (Appendix B's shard
+    pieces before the merge)."""
+    out, ents, off = [], [], 0
+    for v, o, ln in ref.entries.tolist():
+        w = ref.words[o:o + ln].tolist()
+        if (w[0] & 0xC0000000) == 0x80000000:
+            w[0] = 0x80000000 | ((w[0] & 0x3FFFFFFF) + k_chunks)
+        else:
+            w.insert(0, 0x80000000 | k_chunks)
+        ents.append([v, off, len(w)])
+        out += w
+        off += len(w)
+    return np.array(ents, np.uint32).reshape(-1, 3), np.array(out, np.uint32)
+
+
+@pytest.mark.parametrize("k_chunks", [1, 1000, 70_000_000, 100_000_000, 138_000_000])
+def test_row_base_shards(builder, port, k_chunks):
+    """Shard builds with global row ids (row_base = 31k): the emit stage's
+    fast chunk division covers rows < 0x8D3DCB08, larger bases take the
+    exact path; both must match the shifted oracle index."""
+    rng = np.random.default_rng(k_chunks)
+    v = np.concatenate([rng.integers(0, 50, 40_000), np.full(3100, 7), rng.integers(0, 3, 9000)]).astype(np.uint32)
+    got = builder.build(v, row_base=31 * k_chunks)
+    ents, words = _shift_index(port.reference_index(v), k_chunks)
+    assert np.array_equal(got.entries, ents) and np.array_equal(got.words, words)

@@ -1,0 +1,21 @@
+#!/bin/bash
+# One GPU session: parity tests, bench, ncu launch list, ncu --set full of the
+# hot kernels.  Outputs under gpurun_out/$TAG.
+TAG=${TAG:-r1}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+tail -3 $O/pytest_gpu.log
+python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
+cat $O/bench.json
+python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2>>$O/bench.err
+cat $O/bench_ref.json
+python tools/stage_times.py C3 --reps 10 > $O/stages_c3.txt 2>&1
+python tools/stage_times.py C4 --reps 10 > $O/stages_c4.txt 2>&1
+cat $O/stages_c3.txt $O/stages_c4.txt | tail -8
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv \
+  python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
+for C in C4 C3; do
+ncu --set full --clock-control none --import-source on -k regex:"k_hist|k_plan|k_pass|k_emit|k_table" -c 9 \
+  -o $O/full_$C -f python tools/stage_times.py $C --reps 1 > $O/ncu_full_$C.log 2>&1; echo "ncu full $C rc=$?"
+done
