@@ -30,18 +30,16 @@
 
 namespace ndx {
 
-constexpr int kEmitThreads = 256;
+constexpr int kEmitThreads = 128;
 constexpr int kEmitWarps = kEmitThreads / 32;
-constexpr int kEmitIPT = 4;                             // 32-element rounds per warp per tile
-constexpr int kEmitWarpItems = 32 * kEmitIPT;           // 128
-constexpr int kEmitTile = kEmitWarps * kEmitWarpItems;  // 1024
+constexpr int kEmitK = 8;                               // consecutive elements per thread
+constexpr int kEmitTile = kEmitThreads * kEmitK;        // 1024
 constexpr int kHaloL = 32;                              // elements before the tile (carry, prev)
 constexpr int kHaloR = 2;                               // elements after it (next; 16 B multiple)
 constexpr int kEmitBuf = kHaloL + kEmitTile + kHaloR;
-// staging of one tile: per warp 2*kEmitWarpItems words + kEmitWarpItems
-// (value, word offset) table heads
-constexpr int kStageWarp = 4 * kEmitWarpItems;
-constexpr int kStageTile = kEmitWarps * kStageWarp;
+// staging of one tile: 2*kEmitTile words, then kEmitTile table-head values
+// and kEmitTile table-head word offsets (tile-local)
+constexpr int kStageTile = 4 * kEmitTile;
 constexpr size_t kEmitSmem = size_t(2 * kEmitBuf) * 8 + size_t(2 * kStageTile) * 4;
 
 __device__ __forceinline__ uint32_t pkey(uint64_t e) { return uint32_t(e); }
@@ -99,75 +97,120 @@ __device__ __forceinline__ uint32_t div31(uint32_t x) {
   return x / kChunkBits;
 }
 
-// One warp's kEmitWarpItems consecutive elements (tile-local from wl), as
-// kEmitIPT rounds of 32, into the warp's staging area: its words compacted
-// at warp-local offsets (ow) and one (value, warp-local word offset) row per
-// value head (hv, ho).  Returns (words << 16) | value heads.  B[li] is
-// element ts + li, with 32 elements of left halo and 2 of right halo.
+// Phase-1 summary of one thread's kEmitK consecutive elements.
+struct Span {
+  uint64_t P[kEmitK];  // the elements (value | row << 32)
+  uint32_t hmask;      // run heads
+  uint32_t vmask;      // value heads (first element of a value)
+  uint32_t tmask;      // run tails
+  uint32_t pc;         // chunk of the element before P[0]
+  uint32_t acc;        // OR of the bits since the last head (or the span start)
+  uint32_t nwords;     // words this span emits
+  uint32_t first_body; // 1: use the literal; 0: swallowed; else the ones-fill word
+};
+
+// Phase 1: flags and word counts of elements ts+li0 .. ts+li0+kEmitK-1.
+// Only the span's FIRST run can be all-ones: a run that starts inside the
+// span ends inside it with at most kEmitK < 31 elements, or continues into a
+// later span where it is that span's first run.
 template <bool SMALL>
-__device__ __forceinline__ uint32_t warp_tile(const uint64_t* B, const uint64_t* __restrict__ pairs,
-                                              uint32_t n, uint32_t ts, uint32_t wl, uint32_t* ow,
-                                              uint32_t* hv, uint32_t* ho) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t wb = ts + wl;
-  if (wb >= n) return 0;
-  // open run carried into the first round: OR over the preceding elements
-  // with the same (value, chunk) as element wb (all of them are among the
-  // 32 before it: a run has at most 31 elements)
-  uint32_t carry;
-  {
-    const uint64_t e0 = B[wl];
-    const uint32_t v0 = pkey(e0), c0 = div31<SMALL>(prow(e0));
-    const uint64_t q = B[int(wl) - 32 + int(lane)];
-    const uint32_t qrow = prow(q), qc = div31<SMALL>(qrow);
-    const bool m = (wb + lane >= 32) & (pkey(q) == v0) & (qc == c0);
-    carry = __reduce_or_sync(kFull, m ? 1u << (qrow - qc * kChunkBits) : 0u);
-  }
-  const unsigned le = lanemask_le(), lt = lanemask_lt();
-  uint32_t wc = 0, dc = 0;
+__device__ __forceinline__ void span_scan(const uint64_t* B, const uint64_t* __restrict__ pairs,
+                                          uint32_t n, uint32_t ts, uint32_t li0, Span& s) {
+  // 4 x 16 B per thread (the 64 B stride costs 4-way bank conflicts, well
+  // inside the shared-memory budget of ~0.25 wavefronts per element)
+  const uint4* B4 = reinterpret_cast<const uint4*>(B + li0);
 #pragma unroll
-  for (int r = 0; r < kEmitIPT; ++r) {
-    const uint32_t li = wl + r * 32 + lane;
-    const uint32_t e = ts + li;
-    const bool valid = e < n;
-    const uint64_t cur = B[li], prv = B[int(li) - 1], nxt = B[li + 1];
-    const uint32_t v = pkey(cur), row = prow(cur), c = div31<SMALL>(row);
-    const uint32_t pc = div31<SMALL>(prow(prv)), nc = div31<SMALL>(prow(nxt));
-    const bool vhead = valid & ((e == 0) | (pkey(prv) != v));
-    const bool head = vhead | (valid & (pc != c));
-    const bool tail = valid & ((e + 1 == n) | (pkey(nxt) != v) | (nc != c));
-    // run literal: segmented OR-scan over [head lane, lane], plus the open
-    // run's carry when the run began in an earlier round; the scan depth is
-    // the longest run piece ending in this round
-    const unsigned hm = __ballot_sync(kFull, head) & le;
-    const uint32_t hl = 31u - __clz(hm | 1u);
-    const uint32_t span = __reduce_max_sync(kFull, (tail | (lane == 31)) ? lane - hl + 1 : 0u);
-    uint32_t lit = valid ? 1u << (row - c * kChunkBits) : 0u;
-    for (uint32_t d = 1; d < span; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, lit, d);
-      if (lane >= hl + d) lit |= y;
+  for (int p = 0; p < kEmitK / 2; ++p) {
+    const uint4 u = B4[p];
+    s.P[2 * p] = uint64_t(u.x) | (uint64_t(u.y) << 32);
+    s.P[2 * p + 1] = uint64_t(u.z) | (uint64_t(u.w) << 32);
+  }
+  const uint64_t prv = B[int(li0) - 1], nxt = B[li0 + kEmitK];
+  const uint32_t g0 = ts + li0;
+  uint32_t pv = pkey(prv), pc = div31<SMALL>(prow(prv));
+  s.pc = pc;
+  uint32_t hm = 0, vm = 0, gaps = 0, acc = 0;
+#pragma unroll
+  for (int j = 0; j < kEmitK; ++j) {
+    const uint32_t g = g0 + j;
+    const bool valid = g < n;
+    const uint32_t v = pkey(s.P[j]), row = prow(s.P[j]), c = div31<SMALL>(row);
+    const bool vh = valid & ((g == 0) | (v != pv));
+    const bool h = vh | (valid & (c != pc));
+    const uint32_t gap = vh ? c : c - pc - 1;
+    gaps += uint32_t(h & (gap != 0));
+    hm |= uint32_t(h) << j;
+    vm |= uint32_t(vh) << j;
+    acc = (h ? 0u : acc) | (valid ? 1u << (row - c * kChunkBits) : 0u);
+    pv = v;
+    pc = c;
+  }
+  const uint32_t gN = g0 + kEmitK;
+  const uint32_t nvalid = g0 >= n ? 0u : umin(n - g0, uint32_t(kEmitK + 1));
+  const uint32_t valid9 = nvalid >= 32 ? ~0u : ((1u << nvalid) - 1u);
+  const bool hN = (gN < n) & ((pkey(nxt) != pv) | (div31<SMALL>(prow(nxt)) != pc));
+  const uint32_t h9 = hm | (uint32_t(hN) << kEmitK);
+  const uint32_t tm = valid9 & ((1u << kEmitK) - 1u) & ((h9 >> 1) | (~valid9 >> 1));
+  s.hmask = hm;
+  s.vmask = vm;
+  s.tmask = tm;
+  s.acc = acc;
+  s.nwords = gaps + __popc(tm);
+  s.first_body = 1;
+  // the first tail closes a run that began before the span: all-ones check
+  if (tm != 0 && (hm == 0 || __ffs(tm) < __ffs(hm))) {
+    const uint32_t j = __ffs(tm) - 1;
+    const uint64_t te = B[li0 + j];
+    const uint32_t v = pkey(te), row = prow(te);
+    if (row - div31<SMALL>(row) * kChunkBits == kChunkBits - 1 && g0 + j >= 30 &&
+        B[int(li0 + j) - 30] == mkpair(v, row - 30)) {
+      s.first_body = ones_body(pairs, n, g0 + j, v, row);
+      if (s.first_body == 0) s.nwords -= 1;
     }
-    if (hm == 0) lit |= carry;
-    carry = __shfl_sync(kFull, lit, 31);
-    const uint32_t gap = vhead ? c : c - pc - 1;
-    const uint32_t gapw = (head & (gap != 0)) ? (kFillFlag | gap) : 0u;
-    uint32_t body = tail ? lit : 0u;
-    if (body == kLiteralMask) body = ones_body(pairs, n, e, v, row);
-    const unsigned B0 = __ballot_sync(kFull, gapw != 0);
-    const unsigned B1 = __ballot_sync(kFull, body != 0);
-    const unsigned BV = __ballot_sync(kFull, vhead);
-    uint32_t o = wc + __popc(B0 & lt) + __popc(B1 & lt);
-    if (vhead) {
-      const uint32_t h = dc + __popc(BV & lt);
+  }
+}
+
+// Phase 2: write the span's words at tile-local offset o (stage) and its
+// value heads at h (hv: value, ho: tile-local offset of its first word).
+template <bool SMALL>
+__device__ __forceinline__ void span_emit(const Span& s, uint32_t carry, uint32_t o, uint32_t h,
+                                          uint32_t* stage, uint32_t* hv, uint32_t* ho) {
+  uint32_t acc = 0, pc = s.pc;
+  bool first = true;
+#pragma unroll
+  for (int j = 0; j < kEmitK; ++j) {
+    const uint32_t v = pkey(s.P[j]), row = prow(s.P[j]), c = div31<SMALL>(row);
+    const bool hj = (s.hmask >> j) & 1u, vj = (s.vmask >> j) & 1u, tj = (s.tmask >> j) & 1u;
+    if (vj) {
       hv[h] = v;
       ho[h] = o;
+      ++h;
     }
-    if (gapw) ow[o++] = gapw;
-    if (body) ow[o] = body;
-    wc += __popc(B0) + __popc(B1);
-    dc += __popc(BV);
+    const uint32_t gap = vj ? c : c - pc - 1;
+    if (hj & (gap != 0)) stage[o++] = kFillFlag | gap;
+    acc = (hj ? 0u : acc) | (1u << (row - c * kChunkBits));
+    first &= !hj;
+    if (tj) {
+      uint32_t body = first ? (acc | carry) : acc;
+      if (first && s.first_body != 1) body = s.first_body;
+      if (body) stage[o++] = body;
+    }
+    pc = c;
   }
-  return (wc << 16) | dc;
+}
+
+// OR of the bits of the elements before tile-local element wl that share
+// its (value, chunk): the part of wl's run that lies before the warp (at
+// most 30 elements, all inside the 32-element window read here).
+template <bool SMALL>
+__device__ __forceinline__ uint32_t warp_carry(const uint64_t* B, uint32_t ts, uint32_t wl) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t e0 = B[wl];
+  const uint32_t v0 = pkey(e0), c0 = div31<SMALL>(prow(e0));
+  const uint64_t q = B[int(wl) - 32 + int(lane)];
+  const uint32_t qrow = prow(q), qc = div31<SMALL>(qrow);
+  const bool m = (ts + wl + lane >= 32) & (pkey(q) == v0) & (qc == c0);
+  return __reduce_or_sync(kFull, m ? 1u << (qrow - qc * kChunkBits) : 0u);
 }
 
 // Tile schedule: static round-robin (CTA c takes tiles c, c+G, ...).  A
@@ -240,6 +283,8 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
   if (tile < ntiles) fill(tile, 0);
   __syncthreads();
 
+  Span sp;
+  uint32_t ts = 0, carry_in = 0, excl = 0;
   for (int it = 0;; tile += G, ++it) {
     const bool has = tile < ntiles;
     if (!has && pending < 0) break;
@@ -251,25 +296,49 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
         phase ^= 1u << b;
       }
       const uint64_t* B = buf0 + b * kEmitBuf + kHaloL;  // B[li] = pairs[tile * kEmitTile + li]
-      uint32_t* st = stage0 + b * kStageTile + warp * kStageWarp;
-      const uint32_t ts = uint32_t(tile * kEmitTile), wl = uint32_t(warp) * kEmitWarpItems;
-      const uint32_t tot =
-          small_rows
-              ? warp_tile<true>(B, pairs, n32, ts, wl, st, st + 2 * kEmitWarpItems,
-                                st + 3 * kEmitWarpItems)
-              : warp_tile<false>(B, pairs, n32, ts, wl, st, st + 2 * kEmitWarpItems,
-                                 st + 3 * kEmitWarpItems);
-      if (lane == 0) s_wt[b][warp] = tot;
+      ts = uint32_t(tile * kEmitTile);
+      const uint32_t li0 = threadIdx.x * kEmitK;
+      uint32_t wcarry;
+      if (small_rows) {
+        span_scan<true>(B, pairs, n32, ts, li0, sp);
+        wcarry = warp_carry<true>(B, ts, uint32_t(warp) * 32 * kEmitK);
+      } else {
+        span_scan<false>(B, pairs, n32, ts, li0, sp);
+        wcarry = warp_carry<false>(B, ts, uint32_t(warp) * 32 * kEmitK);
+      }
+      // literal carried into each span: segmented OR-scan over the spans'
+      // trailing ORs (bit 31 = the span holds a run head)
+      uint32_t x = (sp.hmask ? 0x80000000u : 0u) | sp.acc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, d);
+        if (lane >= d && !(x >> 31)) x |= y;
+      }
+      const uint32_t incl_lit = (x & kLiteralMask) | ((x >> 31) ? 0u : wcarry);
+      carry_in = __shfl_up_sync(kFull, incl_lit, 1);
+      if (lane == 0) carry_in = wcarry;
+      const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
+      const uint32_t incl = warp_incl_sum(cnt);
+      excl = incl - cnt;
+      if (lane == 31) s_wt[b][warp] = incl;
     }
     __syncthreads();
-    if (has && threadIdx.x == 0) {
-      uint32_t tw = 0, td = 0;
+    if (has) {
+      uint32_t wbase = 0, tot = 0;
 #pragma unroll
       for (int w = 0; w < kEmitWarps; ++w) {
-        tw += s_wt[b][w] >> 16;
-        td += s_wt[b][w] & 0xffffu;
+        const uint32_t t = s_wt[b][w];
+        wbase += w < warp ? t : 0u;
+        tot += t;
       }
-      st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tw) | (uint64_t(td) << 32));
+      if (threadIdx.x == 0)
+        st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32));
+      uint32_t* st = stage0 + b * kStageTile;
+      const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
+      if (small_rows)
+        span_emit<true>(sp, carry_in, o, h, st, st + 2 * kEmitTile, st + 3 * kEmitTile);
+      else
+        span_emit<false>(sp, carry_in, o, h, st, st + 2 * kEmitTile, st + 3 * kEmitTile);
     }
 
     if (pending >= 0) {
@@ -298,18 +367,13 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
       }
       __syncthreads();
       uint64_t W0 = prev_w, D0 = prev_d;
-      uint32_t wbw = 0, wbd = 0, tw = 0, td = 0;
+      uint32_t tw = 0, td = 0;
 #pragma unroll
       for (int w = 0; w < kEmitWarps; ++w) {
         W0 += s_rw[w];
         D0 += s_rd[w];
-        const uint32_t t = s_wt[pb][w];
-        if (w < warp) {
-          wbw += t >> 16;
-          wbd += t & 0xffffu;
-        }
-        tw += t >> 16;
-        td += t & 0xffffu;
+        tw += s_wt[pb][w] >> 16;
+        td += s_wt[pb][w] & 0xffffu;
       }
       prev_w = W0;
       prev_d = D0;
@@ -318,15 +382,12 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
         ctl->words = W0 + tw;
         ctl->distinct = D0 + td;
       }
-      // ---- copy the warp's staged words and table heads out
-      const uint32_t* st = stage0 + pb * kStageTile + warp * kStageWarp;
-      const uint32_t mine = s_wt[pb][warp];
-      const uint32_t nw = mine >> 16, nd = mine & 0xffffu;
-      const uint64_t Ww = W0 + wbw, Dw = D0 + wbd;
-      for (uint32_t j = lane; j < nw; j += 32) words[Ww + j] = st[j];
-      for (uint32_t j = lane; j < nd; j += 32) {
-        values[Dw + j] = st[2 * kEmitWarpItems + j];
-        vstart[Dw + j] = uint32_t(Ww + st[3 * kEmitWarpItems + j]);
+      // ---- copy the tile's staged words and table heads out
+      const uint32_t* st = stage0 + pb * kStageTile;
+      for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[W0 + j] = st[j];
+      for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) {
+        values[D0 + j] = st[2 * kEmitTile + j];
+        vstart[D0 + j] = uint32_t(W0 + st[3 * kEmitTile + j]);
       }
     }
     pending = has ? int64_t(tile) : -1;
