@@ -40,7 +40,7 @@ constexpr int kEmitBuf = kHaloL + kEmitTile + kHaloR;
 // staging of one tile: 2*kEmitTile words, then kEmitTile table-head values
 // and kEmitTile table-head word offsets (tile-local)
 constexpr int kStageTile = 4 * kEmitTile;
-constexpr size_t kEmitSmem = size_t(2 * kEmitBuf) * 8 + size_t(2 * kStageTile) * 4;
+constexpr size_t kEmitSmem = size_t(2 * kEmitBuf) * 8 + size_t(kStageTile) * 4;
 
 __device__ __forceinline__ uint32_t pkey(uint64_t e) { return uint32_t(e); }
 __device__ __forceinline__ uint32_t prow(uint64_t e) { return uint32_t(e >> 32); }
@@ -97,67 +97,26 @@ __device__ __forceinline__ uint32_t div31(uint32_t x) {
   return x / kChunkBits;
 }
 
-// Phase-1 summary of one thread's kEmitK consecutive elements.
+// Phase-1 summary of one thread's kEmitK consecutive elements ("span").
 struct Span {
-  uint64_t P[kEmitK];  // the elements (value | row << 32)
-  uint32_t hmask;      // run heads
-  uint32_t vmask;      // value heads (first element of a value)
-  uint32_t tmask;      // run tails
-  uint32_t pc;         // chunk of the element before P[0]
-  uint32_t acc;        // OR of the bits since the last head (or the span start)
-  uint32_t nwords;     // words this span emits
-  uint32_t first_body; // 1: use the literal; 0: swallowed; else the ones-fill word
+  uint32_t pk[kEmitK];  // per element: gap-fill length (0: no gap word), << 5 | row % 31 when SMALL
+  uint32_t hmask;       // run heads
+  uint32_t vmask;       // value heads (first element of a value)
+  uint32_t tmask;       // run tails
+  uint32_t acc;         // OR of the bits since the last head (or the span start)
+  uint32_t nwords;      // words this span emits
+  uint32_t first_body;  // 1: literal; 0: swallowed; else the ones-fill word (first run only)
 };
 
-// Phase 1: flags and word counts of elements ts+li0 .. ts+li0+kEmitK-1.
-// Only the span's FIRST run can be all-ones: a run that starts inside the
-// span ends inside it with at most kEmitK < 31 elements, or continues into a
-// later span where it is that span's first run.
+// All-ones check of the span's first run when it began before the span
+// (the only run of a span that can be all-ones: one that starts inside the
+// span either ends inside it with at most kEmitK < 31 elements, or continues
+// into a later span where it is that span's first run).
 template <bool SMALL>
-__device__ __forceinline__ void span_scan(const uint64_t* B, const uint64_t* __restrict__ pairs,
-                                          uint32_t n, uint32_t ts, uint32_t li0, Span& s) {
-  // 4 x 16 B per thread (the 64 B stride costs 4-way bank conflicts, well
-  // inside the shared-memory budget of ~0.25 wavefronts per element)
-  const uint4* B4 = reinterpret_cast<const uint4*>(B + li0);
-#pragma unroll
-  for (int p = 0; p < kEmitK / 2; ++p) {
-    const uint4 u = B4[p];
-    s.P[2 * p] = uint64_t(u.x) | (uint64_t(u.y) << 32);
-    s.P[2 * p + 1] = uint64_t(u.z) | (uint64_t(u.w) << 32);
-  }
-  const uint64_t prv = B[int(li0) - 1], nxt = B[li0 + kEmitK];
-  const uint32_t g0 = ts + li0;
-  uint32_t pv = pkey(prv), pc = div31<SMALL>(prow(prv));
-  s.pc = pc;
-  uint32_t hm = 0, vm = 0, gaps = 0, acc = 0;
-#pragma unroll
-  for (int j = 0; j < kEmitK; ++j) {
-    const uint32_t g = g0 + j;
-    const bool valid = g < n;
-    const uint32_t v = pkey(s.P[j]), row = prow(s.P[j]), c = div31<SMALL>(row);
-    const bool vh = valid & ((g == 0) | (v != pv));
-    const bool h = vh | (valid & (c != pc));
-    const uint32_t gap = vh ? c : c - pc - 1;
-    gaps += uint32_t(h & (gap != 0));
-    hm |= uint32_t(h) << j;
-    vm |= uint32_t(vh) << j;
-    acc = (h ? 0u : acc) | (valid ? 1u << (row - c * kChunkBits) : 0u);
-    pv = v;
-    pc = c;
-  }
-  const uint32_t gN = g0 + kEmitK;
-  const uint32_t nvalid = g0 >= n ? 0u : umin(n - g0, uint32_t(kEmitK + 1));
-  const uint32_t valid9 = nvalid >= 32 ? ~0u : ((1u << nvalid) - 1u);
-  const bool hN = (gN < n) & ((pkey(nxt) != pv) | (div31<SMALL>(prow(nxt)) != pc));
-  const uint32_t h9 = hm | (uint32_t(hN) << kEmitK);
-  const uint32_t tm = valid9 & ((1u << kEmitK) - 1u) & ((h9 >> 1) | (~valid9 >> 1));
-  s.hmask = hm;
-  s.vmask = vm;
-  s.tmask = tm;
-  s.acc = acc;
-  s.nwords = gaps + __popc(tm);
+__device__ __forceinline__ void first_run_check(const uint64_t* B, const uint64_t* __restrict__ pairs,
+                                                uint32_t n, uint32_t g0, uint32_t li0, Span& s) {
   s.first_body = 1;
-  // the first tail closes a run that began before the span: all-ones check
+  const uint32_t tm = s.tmask, hm = s.hmask;
   if (tm != 0 && (hm == 0 || __ffs(tm) < __ffs(hm))) {
     const uint32_t j = __ffs(tm) - 1;
     const uint64_t te = B[li0 + j];
@@ -170,32 +129,109 @@ __device__ __forceinline__ void span_scan(const uint64_t* B, const uint64_t* __r
   }
 }
 
-// Phase 2: write the span's words at tile-local offset o (stage) and its
-// value heads at h (hv: value, ho: tile-local offset of its first word).
-template <bool SMALL>
-__device__ __forceinline__ void span_emit(const Span& s, uint32_t carry, uint32_t o, uint32_t h,
-                                          uint32_t* stage, uint32_t* hv, uint32_t* ho) {
-  uint32_t acc = 0, pc = s.pc;
-  bool first = true;
+// Phase 1: flags, gap lengths and word count of elements ts+li0 ..
+// ts+li0+kEmitK-1.  FULL: the span and the element after it exist and the
+// span does not start at element 0 (every tile that arrives by bulk copy).
+template <bool SMALL, bool FULL>
+__device__ __forceinline__ void span_scan(const uint64_t* B, const uint64_t* __restrict__ pairs,
+                                          uint32_t n, uint32_t ts, uint32_t li0, Span& s) {
+  // 4 x 16 B per thread (the 64 B stride costs 4-way bank conflicts, well
+  // inside the shared-memory budget of ~0.25 wavefronts per element)
+  uint64_t P[kEmitK];
+  const uint4* B4 = reinterpret_cast<const uint4*>(B + li0);
+#pragma unroll
+  for (int p = 0; p < kEmitK / 2; ++p) {
+    const uint4 u = B4[p];
+    P[2 * p] = uint64_t(u.x) | (uint64_t(u.y) << 32);
+    P[2 * p + 1] = uint64_t(u.z) | (uint64_t(u.w) << 32);
+  }
+  const uint64_t prv = B[int(li0) - 1], nxt = B[li0 + kEmitK];
+  const uint32_t g0 = ts + li0;
+  uint32_t pv = pkey(prv), pc = div31<SMALL>(prow(prv));
+  uint32_t hm = 0, vm = 0, gaps = 0, acc = 0;
 #pragma unroll
   for (int j = 0; j < kEmitK; ++j) {
-    const uint32_t v = pkey(s.P[j]), row = prow(s.P[j]), c = div31<SMALL>(row);
-    const bool hj = (s.hmask >> j) & 1u, vj = (s.vmask >> j) & 1u, tj = (s.tmask >> j) & 1u;
-    if (vj) {
-      hv[h] = v;
+    const uint32_t v = pkey(P[j]), row = prow(P[j]), c = div31<SMALL>(row);
+    const uint32_t bp = row - c * kChunkBits;
+    bool vh = v != pv, h = vh | (c != pc);
+    if (!FULL) {
+      const uint32_t g = g0 + j;
+      const bool valid = g < n;
+      vh = valid & (vh | (g == 0));
+      h = valid & (h | (g == 0));
+    }
+    const uint32_t gap = h ? (vh ? c : c - pc - 1) : 0u;
+    gaps += gap != 0;
+    s.pk[j] = SMALL ? (gap << 5) | bp : gap;  // SMALL: chunks < 2^27
+    hm |= uint32_t(h) << j;
+    vm |= uint32_t(vh) << j;
+    acc = (h ? 0u : acc) | (1u << bp);
+    pv = v;
+    pc = c;
+  }
+  const bool hN = (pkey(nxt) != pv) | (div31<SMALL>(prow(nxt)) != pc);
+  uint32_t tm;
+  if (FULL) {
+    tm = (hm >> 1) | (uint32_t(hN) << (kEmitK - 1));
+  } else {
+    const uint32_t nvalid = g0 >= n ? 0u : umin(n - g0, uint32_t(kEmitK + 1));
+    const uint32_t valid9 = (1u << nvalid) - 1u;
+    const uint32_t h9 = hm | (uint32_t(hN) << kEmitK);
+    tm = valid9 & ((1u << kEmitK) - 1u) & ((h9 >> 1) | (~valid9 >> 1));
+  }
+  s.hmask = hm;
+  s.vmask = vm;
+  s.tmask = tm;
+  s.acc = acc;
+  s.nwords = gaps + __popc(tm);
+  first_run_check<SMALL>(B, pairs, n, g0, li0, s);
+}
+
+// Phase 2: write the span's words at tile-local offset o of `stage` and its
+// value heads at h (hv: value, ho: tile-local offset of the value's first
+// word).  `carry` is the OR of the span's first run before the span, so the
+// running literal simply starts from it.
+template <bool SMALL>
+__device__ __forceinline__ uint32_t gap_of(uint32_t pk) {
+  return SMALL ? pk >> 5 : pk;
+}
+template <bool SMALL>
+__device__ __forceinline__ uint32_t bit_of(uint32_t pk, uint64_t e) {
+  if (SMALL) return 1u << (pk & 31u);
+  const uint32_t row = prow(e);
+  return 1u << (row - (row / kChunkBits) * kChunkBits);
+}
+
+template <bool SMALL>
+__device__ __forceinline__ void span_emit(const Span& s, const uint64_t* Bs, uint32_t carry,
+                                          uint32_t o, uint32_t h, uint32_t* stage, uint32_t* hv,
+                                          uint32_t* ho) {
+  uint32_t acc = carry;
+  if (s.vmask == 0 && s.first_body == 1) {
+#pragma unroll
+    for (int j = 0; j < kEmitK; ++j) {
+      const uint32_t gap = gap_of<SMALL>(s.pk[j]), bit = bit_of<SMALL>(s.pk[j], Bs[j]);
+      if (gap) stage[o++] = kFillFlag | gap;
+      acc = ((s.hmask >> j) & 1u) ? bit : (acc | bit);
+      if ((s.tmask >> j) & 1u) stage[o++] = acc;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < kEmitK; ++j) {
+    const uint32_t gap = gap_of<SMALL>(s.pk[j]), bit = bit_of<SMALL>(s.pk[j], Bs[j]);
+    if ((s.vmask >> j) & 1u) {
+      hv[h] = pkey(Bs[j]);
       ho[h] = o;
       ++h;
     }
-    const uint32_t gap = vj ? c : c - pc - 1;
-    if (hj & (gap != 0)) stage[o++] = kFillFlag | gap;
-    acc = (hj ? 0u : acc) | (1u << (row - c * kChunkBits));
-    first &= !hj;
-    if (tj) {
-      uint32_t body = first ? (acc | carry) : acc;
-      if (first && s.first_body != 1) body = s.first_body;
+    if (gap) stage[o++] = kFillFlag | gap;
+    acc = ((s.hmask >> j) & 1u) ? bit : (acc | bit);
+    if ((s.tmask >> j) & 1u) {
+      const bool first = (s.hmask & ((2u << j) - 1u)) == 0;
+      const uint32_t body = (first && s.first_body != 1) ? s.first_body : acc;
       if (body) stage[o++] = body;
     }
-    pc = c;
   }
 }
 
@@ -213,21 +249,32 @@ __device__ __forceinline__ uint32_t warp_carry(const uint64_t* B, uint32_t ts, u
   return __reduce_or_sync(kFull, m ? 1u << (qrow - qc * kChunkBits) : 0u);
 }
 
-// Tile schedule: static round-robin (CTA c takes tiles c, c+G, ...).  A
-// tile's global offsets are the CTA's own previous tile's offsets plus the
-// published aggregates of the G tiles in between -- one block-wide read,
-// never a serial look-back chain.  The CTA computes tile k (publishing its
-// aggregate) BEFORE it writes tile k-1 out, so by the time it needs the
-// aggregates below tile k-1 the other CTAs have had a whole tile's worth of
-// time to publish them.  All G CTAs are co-resident (cooperative launch); a
-// tile only waits on smaller tiles, whose owners publish before they wait,
-// so the schedule cannot deadlock.
+// Tile schedule: tiles are handed out in order by an atomic counter.  A
+// tile's global offsets are the offsets of this CTA's previous tile plus the
+// published aggregates of the tiles in between (about one per CTA) -- a
+// block-wide read, never a serial look-back chain.  The CTA computes tile
+// k's counts (publishing its aggregate) BEFORE it writes tile k-1 out, so by
+// the time it needs the aggregates below tile k-1 the CTAs that took them
+// have had a whole phase to publish.  All CTAs are co-resident (cooperative
+// launch); a tile waits only on smaller tiles, taken earlier by CTAs that
+// publish before they wait, so the schedule cannot deadlock.
 //
-// The next tile's pairs arrive by one bulk async copy (TMA, mbarrier
-// completion) into the other shared buffer while this tile is processed.
+// Tiles whose halo lies inside [0, n) arrive by one bulk async copy (TMA,
+// mbarrier completion) issued a phase ahead; the first and last ones are
+// gathered by the threads.
 constexpr uint64_t kAggReady = 1ull << 63;
 
-__global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __restrict__ pairs,
+template <bool SMALL>
+__device__ __forceinline__ void tile_phase1(bool full, const uint64_t* B,
+                                            const uint64_t* __restrict__ pairs, uint32_t n,
+                                            uint32_t ts, uint32_t li0, Span& sp) {
+  if (full)
+    span_scan<SMALL, true>(B, pairs, n, ts, li0, sp);
+  else
+    span_scan<SMALL, false>(B, pairs, n, ts, li0, sp);
+}
+
+__global__ __launch_bounds__(kEmitThreads, 6) void k_emit(const uint64_t* __restrict__ pairs,
                                                           uint64_t n, Ctl* ctl,
                                                           uint32_t* __restrict__ words,
                                                           uint32_t* __restrict__ vstart,
@@ -235,36 +282,32 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
                                                           uint64_t* agg, int bulk_ok) {
   extern __shared__ __align__(16) unsigned char emit_smem[];
   uint64_t* buf0 = reinterpret_cast<uint64_t*>(emit_smem);
-  uint32_t* stage0 = reinterpret_cast<uint32_t*>(buf0 + 2 * kEmitBuf);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(buf0 + 2 * kEmitBuf);
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ uint32_t s_wt[2][kEmitWarps];
   __shared__ uint32_t s_rw[kEmitWarps], s_rd[kEmitWarps];
+  __shared__ uint32_t s_tile[2];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t ntiles = (n + kEmitTile - 1) / kEmitTile;
-  const uint64_t G = gridDim.x;
+  const uint32_t ntiles = uint32_t((n + kEmitTile - 1) / kEmitTile);
   const uint32_t n32 = uint32_t(n);  // n < 2^31 (checked by the launcher)
   const bool small_rows = ctl->row_hi < kDiv31FastLimit;
+  uint32_t* ctr = &ctl->tile_ctr[0];
 
-  // Tiles whose halo range lies inside [0, n) arrive by bulk copy; the
-  // first and the last ones are gathered by the threads.
-  auto by_bulk = [&](uint64_t t) -> bool {
-    return bulk_ok && t > 0 && (t + 1) * kEmitTile + kHaloR <= n;
+  auto by_bulk = [&](uint32_t t) -> bool {
+    return bulk_ok && t > 0 && uint64_t(t + 1) * kEmitTile + kHaloR <= n;
   };
-  auto fill = [&](uint64_t t, int b) {
+  auto bulk_fill = [&](uint32_t t, int b) {  // one thread
+    fence_proxy_async_smem();
+    mbar_expect_tx(&bar[b], kEmitBuf * 8);
+    bulk_g2s(buf0 + b * kEmitBuf, pairs + (int64_t(t) * kEmitTile - kHaloL), kEmitBuf * 8, &bar[b]);
+  };
+  auto manual_fill = [&](uint32_t t, int b) {  // all threads
     uint64_t* dst = buf0 + b * kEmitBuf;
-    const int64_t g0 = int64_t(t * kEmitTile) - kHaloL;
-    if (by_bulk(t)) {
-      if (threadIdx.x == 0) {
-        fence_proxy_async_smem();
-        mbar_expect_tx(&bar[b], kEmitBuf * 8);
-        bulk_g2s(dst, pairs + g0, kEmitBuf * 8, &bar[b]);
-      }
-    } else {
-      for (int j = threadIdx.x; j < kEmitBuf; j += kEmitThreads) {
-        const int64_t g = g0 + j;
-        dst[j] = (g >= 0 && uint64_t(g) < n) ? __ldg(pairs + g) : 0ull;
-      }
+    const int64_t g0 = int64_t(t) * kEmitTile - kHaloL;
+    for (int j = threadIdx.x; j < kEmitBuf; j += kEmitThreads) {
+      const int64_t g = g0 + j;
+      dst[j] = (g >= 0 && uint64_t(g) < n) ? __ldg(pairs + g) : 0ull;
     }
   };
 
@@ -272,38 +315,41 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
+    const uint32_t t = atomicAdd(ctr, 1u);
+    s_tile[0] = t;
+    if (t < ntiles && by_bulk(t)) bulk_fill(t, 0);
   }
   __syncthreads();
 
   uint64_t prev_w = 0, prev_d = 0;  // exclusive offsets of this CTA's last written tile
   int64_t prev_tile = -1;
-  int64_t pending = -1;             // computed, not yet written
+  int64_t pending = -1;             // counted, not yet written
   uint32_t phase = 0;
-  uint64_t tile = blockIdx.x;
-  if (tile < ntiles) fill(tile, 0);
-  __syncthreads();
-
   Span sp;
-  uint32_t ts = 0, carry_in = 0, excl = 0;
-  for (int it = 0;; tile += G, ++it) {
+  uint32_t carry_in = 0, excl = 0;
+  for (int it = 0;; ++it) {
+    const int b = it & 1;
+    const uint32_t tile = s_tile[b];
     const bool has = tile < ntiles;
     if (!has && pending < 0) break;
-    const int b = it & 1;
+    const bool full = has && by_bulk(tile);
+    const uint64_t* B = buf0 + b * kEmitBuf + kHaloL;  // B[li] = pairs[tile * kEmitTile + li]
+    const uint32_t ts = tile * kEmitTile, li0 = threadIdx.x * kEmitK;
     if (has) {
-      if (tile + G < ntiles) fill(tile + G, b ^ 1);
-      if (by_bulk(tile)) {
+      if (full) {
         mbar_wait(&bar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
+      } else {
+        manual_fill(tile, b);
+        __syncthreads();
       }
-      const uint64_t* B = buf0 + b * kEmitBuf + kHaloL;  // B[li] = pairs[tile * kEmitTile + li]
-      ts = uint32_t(tile * kEmitTile);
-      const uint32_t li0 = threadIdx.x * kEmitK;
+      // ---- phase 1: counts and carries
       uint32_t wcarry;
       if (small_rows) {
-        span_scan<true>(B, pairs, n32, ts, li0, sp);
+        tile_phase1<true>(full, B, pairs, n32, ts, li0, sp);
         wcarry = warp_carry<true>(B, ts, uint32_t(warp) * 32 * kEmitK);
       } else {
-        span_scan<false>(B, pairs, n32, ts, li0, sp);
+        tile_phase1<false>(full, B, pairs, n32, ts, li0, sp);
         wcarry = warp_carry<false>(B, ts, uint32_t(warp) * 32 * kEmitK);
       }
       // literal carried into each span: segmented OR-scan over the spans'
@@ -323,26 +369,21 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
       if (lane == 31) s_wt[b][warp] = incl;
     }
     __syncthreads();
-    if (has) {
-      uint32_t wbase = 0, tot = 0;
+    if (threadIdx.x == 0) {
+      if (has) {
+        uint32_t tot = 0;
 #pragma unroll
-      for (int w = 0; w < kEmitWarps; ++w) {
-        const uint32_t t = s_wt[b][w];
-        wbase += w < warp ? t : 0u;
-        tot += t;
-      }
-      if (threadIdx.x == 0)
+        for (int w = 0; w < kEmitWarps; ++w) tot += s_wt[b][w];
         st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32));
-      uint32_t* st = stage0 + b * kStageTile;
-      const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
-      if (small_rows)
-        span_emit<true>(sp, carry_in, o, h, st, st + 2 * kEmitTile, st + 3 * kEmitTile);
-      else
-        span_emit<false>(sp, carry_in, o, h, st, st + 2 * kEmitTile, st + 3 * kEmitTile);
+      }
+      // take the next tile; its bulk copy overlaps the rest of this one
+      const uint32_t nt = has ? atomicAdd(ctr, 1u) : ntiles;
+      s_tile[b ^ 1] = nt;
+      if (nt < ntiles && by_bulk(nt)) bulk_fill(nt, b ^ 1);
     }
 
     if (pending >= 0) {
-      // ---- write the previous tile: global offsets first
+      // ---- write the previous tile out: global offsets first
       const int pb = b ^ 1;
       const uint64_t pt = uint64_t(pending);
       const uint64_t lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
@@ -382,16 +423,26 @@ __global__ __launch_bounds__(kEmitThreads, 4) void k_emit(const uint64_t* __rest
         ctl->words = W0 + tw;
         ctl->distinct = D0 + td;
       }
-      // ---- copy the tile's staged words and table heads out
-      const uint32_t* st = stage0 + pb * kStageTile;
-      for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[W0 + j] = st[j];
+      for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[W0 + j] = stage[j];
       for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) {
-        values[D0 + j] = st[2 * kEmitTile + j];
-        vstart[D0 + j] = uint32_t(W0 + st[3 * kEmitTile + j]);
+        values[D0 + j] = stage[2 * kEmitTile + j];
+        vstart[D0 + j] = uint32_t(W0 + stage[3 * kEmitTile + j]);
       }
     }
+    __syncthreads();  // the staging area is free again; s_tile[b^1] visible
+
+    if (has) {
+      // ---- phase 2: this tile's words into the staging area
+      uint32_t wbase = 0;
+#pragma unroll
+      for (int w = 0; w < kEmitWarps; ++w) wbase += w < warp ? s_wt[b][w] : 0u;
+      const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
+      if (small_rows)
+        span_emit<true>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile, stage + 3 * kEmitTile);
+      else
+        span_emit<false>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile, stage + 3 * kEmitTile);
+    }
     pending = has ? int64_t(tile) : -1;
-    __syncthreads();
   }
 }
 
