@@ -38,14 +38,17 @@ def _stale(out: str, srcs: list[str]) -> bool:
 
 
 def build_ndx(force: bool = False) -> str:
-    out = os.path.join(LIB, "libndx.so")
+    # NDX_OUT / NDX_DEFINES build experiment variants next to libndx.so
+    # (selected at load time with NDX_LIB); the product is always libndx.so.
+    out = os.path.join(LIB, os.environ.get("NDX_OUT", "libndx.so"))
+    defines = os.environ.get("NDX_DEFINES", "").split()
     srcs = sorted(glob.glob(os.path.join(CSRC, "kernels", "*.cu")))
     deps = srcs + glob.glob(os.path.join(CSRC, "kernels", "*.cuh")) + [os.path.join(INC, "ndx.h")]
     if force or _stale(out, deps):
         os.makedirs(LIB, exist_ok=True)
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-v" if os.environ.get("NDX_PTXAS_V") else "-O3",
-              "--expt-relaxed-constexpr", "-cudart", "static", "-shared", "-I" + INC,
+              "--expt-relaxed-constexpr", "-cudart", "static", "-shared", "-I" + INC, *defines,
               "-o", out, *srcs])
     return out
 

@@ -33,9 +33,18 @@
 
 namespace ndx {
 
-constexpr int kSortThreads = 256;
+#ifndef NDX_SORT_THREADS
+#define NDX_SORT_THREADS 256
+#endif
+#ifndef NDX_SORT_IPT
+#define NDX_SORT_IPT 16
+#endif
+#ifndef NDX_SORT_MINB
+#define NDX_SORT_MINB 3
+#endif
+constexpr int kSortThreads = NDX_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortIPT = 16;                          // items per thread
+constexpr int kSortIPT = NDX_SORT_IPT;                // items per thread
 constexpr int kSortWarpItems = 32 * kSortIPT;         // 512
 constexpr int kSortTile = kSortThreads * kSortIPT;    // 4096 pairs
 
@@ -321,18 +330,24 @@ struct TileCtx {
 };
 
 // Exclusive count of digit d over all tiles before `tile` (decoupled
-// look-back, four predecessor statuses in flight at a time).
+// look-back, kLookbackWidth predecessor statuses in flight at a time: the
+// look-back depth grows with the number of tiles in flight, so each step
+// covers several predecessors with one round trip).
+#ifndef NDX_LOOKBACK_WIDTH
+#define NDX_LOOKBACK_WIDTH 4
+#endif
+constexpr int kLookbackWidth = NDX_LOOKBACK_WIDTH;
 __device__ __forceinline__ uint64_t lookback(const uint64_t* st, uint64_t tile, uint32_t nb,
                                              uint32_t d, uint32_t epoch) {
   uint64_t excl = 0;
   int64_t t0 = int64_t(tile) - 1;
   while (t0 >= 0) {
-    uint64_t s[4];
+    uint64_t s[kLookbackWidth];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < kLookbackWidth; ++j)
       s[j] = t0 - j >= 0 ? ld_relaxed_u64(&st[uint64_t(t0 - j) * nb + d]) : 0ull;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kLookbackWidth; ++j) {
       if (t0 - j < 0) return excl;
       while (!st_ready(s[j], epoch)) {
         __nanosleep(64);
@@ -341,7 +356,7 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* st, uint64_t tile, 
       excl += s[j] & kStValue;
       if ((s[j] & (3ull << 38)) == kStPrefix) return excl;
     }
-    t0 -= 4;
+    t0 -= kLookbackWidth;
   }
   return excl;
 }
@@ -435,7 +450,9 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     const uint32_t c = t.cnt[d], local = t.gbase[d];
     uint64_t excl = 0;
     if (tile > 0) {
+#ifndef NDX_EXP_NOLOOKBACK
       excl = lookback(t.status, tile, NB, d, t.epoch);
+#endif
       st_relaxed_u64(&st[d], st_word(t.epoch, kStPrefix, excl + c));
     }
 #pragma unroll
@@ -494,7 +511,7 @@ __device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint3
 // One stable scatter pass over persistent CTAs.  Pass q writes X iff
 // (P-1-q) is even, so the last pass lands in X.
 template <int MAXB>
-__global__ __launch_bounds__(kSortThreads, 3) void k_pass(SortArgs a, int which) {
+__global__ __launch_bounds__(kSortThreads, NDX_SORT_MINB) void k_pass(SortArgs a, int which) {
   if (which < 0 && blockIdx.x == 0 && threadIdx.x == 0)
     a.ctl->row_hi = a.row_base + uint32_t(a.n - 1);  // read by the emit stage
   PassInfo pi;
@@ -567,6 +584,10 @@ static int launch_cfg(LaunchCfg** out) {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_pass<8>, kSortThreads,
                                                            sb)))
       return e;
+#ifdef NDX_SORT_OCC_CAP
+    c.occ_wide = umin(c.occ_wide, NDX_SORT_OCC_CAP);
+    c.occ_byte = umin(c.occ_byte, NDX_SORT_OCC_CAP);
+#endif
     if (c.occ_wide < 1) c.occ_wide = 1;
     if (c.occ_byte < 1) c.occ_byte = 1;
     c.ready = true;
