@@ -114,6 +114,41 @@ int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart,
                   void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Multi-GPU build: shards of rows [S_g, S_{g+1}),
+ * S_g = 0 mod 31, are built with row_base = S_g; the pieces are then merged.
+ * ------------------------------------------------------------------------- */
+/* Per value of one shard's local index. */
+typedef struct {
+  uint32_t value;
+  uint32_t f;         /* first chunk holding the value in this shard         */
+  uint32_t l;         /* last chunk                                          */
+  uint32_t a;         /* ones-fill length of the body's first word, or 0     */
+  uint32_t z;         /* ones-fill length of the body's last word, or 0      */
+  uint32_t body_off;  /* local word offset of the body (after the leading    */
+  uint32_t body_len;  /*   zero-fill, which is `skip` words long: 0 or 1)    */
+  uint32_t skip;
+} ndx_shard_meta;
+
+/* One piece of the merged index: `lead` (if nonzero) at dst, then src_len
+ * words from src_off of the shard's (staged) words. */
+typedef struct {
+  uint64_t dst;
+  uint32_t src_off;
+  uint32_t src_len;
+  uint32_t lead;
+  uint32_t pad;
+} ndx_piece;
+
+/* meta[d] for each entry d of a local index built by the four stages (pairs
+ * are that build's sorted pairs). */
+int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
+                       uint64_t n_entries, const uint32_t* d_words, ndx_shard_meta* d_meta,
+                       void* stream);
+/* Copies every piece to out (the merged words). */
+int ndx_wah_assemble(const uint32_t* d_src, const ndx_piece* d_pieces, uint64_t n_pieces,
+                     uint32_t* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Device primitives behind the reference's public WAH device API
  * (p/core/include/ndactor/wah_device.hpp:17-50).
  * ------------------------------------------------------------------------- */

@@ -1,0 +1,109 @@
+// Multi-GPU build: per-shard metadata and the final word assembly
+// (SURVEY.md section 8(e), Appendix B).
+//
+// Shard g builds rows [S_g, S_{g+1}) with S_g = 0 (mod 31) and global row
+// ids (row_base = S_g), so no 31-row chunk straddles two shards and each
+// local index is canonical except for its leading zero-fill.  The merge only
+// touches the ends of each value's piece:
+//   * the local leading zero-fill is replaced by the cross-shard gap fill
+//     (or dropped / kept for the first piece),
+//   * ones-fills that meet at gap 0 are fused into one.
+// The planning over the (small) metadata runs on the host
+// (csrc/runtime/merge_plan.cpp); these kernels do the per-value metadata and
+// the copy of every piece to its final position.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../../include/ndx.h"
+#include "common.cuh"
+
+namespace ndx {
+
+__device__ __forceinline__ uint32_t fill_chunks(uint32_t w) { return w & kLenMask; }
+__device__ __forceinline__ bool is_zero_fill(uint32_t w) { return (w & 0xC0000000u) == kFillFlag; }
+__device__ __forceinline__ bool is_ones_fill(uint32_t w) { return (w & 0xC0000000u) == 0xC0000000u; }
+
+// First index in pairs[0, n) whose key is >= v (keys ascending).
+__device__ __forceinline__ uint64_t lower_key(const uint64_t* pairs, uint64_t n, uint32_t v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (uint32_t(__ldg(pairs + mid)) < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One thread per value of the local index: first / last chunk (from the
+// sorted pairs), leading and trailing ones-fill of the body, and the body
+// range (the words after the local leading zero-fill).
+__global__ void k_shard_meta(const uint64_t* __restrict__ pairs, uint64_t n,
+                             const uint32_t* __restrict__ entries, uint64_t D,
+                             const uint32_t* __restrict__ words, ndx_shard_meta* __restrict__ meta) {
+  for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < D;
+       d += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = entries[3 * d], off = entries[3 * d + 1], len = entries[3 * d + 2];
+    const uint64_t lo = lower_key(pairs, n, v);
+    const uint64_t hi = v == 0xffffffffu ? n : lower_key(pairs, n, v + 1);
+    ndx_shard_meta m;
+    m.value = v;
+    m.f = uint32_t(__ldg(pairs + lo) >> 32) / kChunkBits;
+    m.l = uint32_t(__ldg(pairs + hi - 1) >> 32) / kChunkBits;
+    m.skip = is_zero_fill(words[off]) ? 1u : 0u;
+    m.body_off = off + m.skip;
+    m.body_len = len - m.skip;
+    const uint32_t first = words[m.body_off], last = words[m.body_off + m.body_len - 1];
+    m.a = is_ones_fill(first) ? fill_chunks(first) : 0u;
+    m.z = is_ones_fill(last) ? fill_chunks(last) : 0u;
+    meta[d] = m;
+  }
+}
+
+// One warp per piece: the optional lead word, then src_len words copied from
+// the piece's shard words (already offset into the staging buffer).
+__global__ void k_assemble(const uint32_t* __restrict__ src, const ndx_piece* __restrict__ pieces,
+                           uint64_t npieces, uint32_t* __restrict__ out) {
+  const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t p = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p < npieces; p += warps) {
+    const ndx_piece pc = pieces[p];
+    uint32_t* dst = out + pc.dst;
+    if (pc.lead) {
+      if (lane == 0) dst[0] = pc.lead;
+      ++dst;
+    }
+    const uint32_t* s = src + pc.src_off;
+    for (uint32_t j = lane; j < pc.src_len; j += 32) dst[j] = __ldg(s + j);
+  }
+}
+
+}  // namespace ndx
+
+using namespace ndx;
+
+extern "C" {
+
+int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
+                       uint64_t n_entries, const uint32_t* d_words, ndx_shard_meta* d_meta,
+                       void* stream) {
+  if (n_entries == 0) return 0;
+  if (!d_pairs || !d_entries || !d_words || !d_meta || n == 0) return NDX_E_INVALID;
+  const int grid = int(umin<uint64_t>((n_entries + 255) / 256, 4096));
+  k_shard_meta<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_pairs, n, d_entries,
+                                                                     n_entries, d_words, d_meta);
+  return cudaGetLastError();
+}
+
+int ndx_wah_assemble(const uint32_t* d_src, const ndx_piece* d_pieces, uint64_t n_pieces,
+                     uint32_t* d_out, void* stream) {
+  if (n_pieces == 0) return 0;
+  if (!d_src || !d_pieces || !d_out) return NDX_E_INVALID;
+  const int grid = int(umin<uint64_t>((n_pieces + 7) / 8, 148 * 16));
+  k_assemble<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_src, d_pieces, n_pieces, d_out);
+  return cudaGetLastError();
+}
+
+}  // extern "C"

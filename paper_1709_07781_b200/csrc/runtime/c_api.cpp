@@ -9,6 +9,7 @@
 #include "ndactor/compute_actor.hpp"
 #include "ndactor/wah_device.hpp"
 #include "ndactor/wah_io.hpp"
+#include "ndactor/wah_shard.hpp"
 #include "ndx.h"
 
 using namespace ndactor;
@@ -257,6 +258,41 @@ int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_
       idx.entries[i] = wah::IndexEntry{entries[3 * i], entries[3 * i + 1], entries[3 * i + 2]};
     idx.words.assign(words, words + n_words);
     wah::write_index_file(path, idx);
+    return 0;
+  });
+}
+
+int ndactor_shard_bounds(uint64_t n, uint32_t shards, uint64_t* bounds) {
+  return guarded([&] {
+    const auto b = wah::shard_bounds(n, shards);
+    std::memcpy(bounds, b.data(), b.size() * sizeof(uint64_t));
+    return 0;
+  });
+}
+
+int ndactor_merge_plan(uint32_t shards, const ndx_shard_meta* metas, const uint64_t* counts,
+                       uint32_t* entries, ndx_piece* pieces, uint64_t* n_entries,
+                       uint64_t* n_words) {
+  return guarded([&] {
+    std::vector<std::span<const ndx_shard_meta>> sh(shards);
+    std::uint64_t off = 0;
+    for (uint32_t g = 0; g < shards; ++g) {
+      sh[g] = std::span<const ndx_shard_meta>(metas + off, counts[g]);
+      off += counts[g];
+    }
+    const wah::MergePlan plan = wah::plan_merge(sh);
+    for (std::size_t i = 0; i < plan.entries.size(); ++i) {
+      entries[3 * i] = plan.entries[i].value;
+      entries[3 * i + 1] = plan.entries[i].offset;
+      entries[3 * i + 2] = plan.entries[i].length;
+    }
+    off = 0;
+    for (uint32_t g = 0; g < shards; ++g) {
+      std::memcpy(pieces + off, plan.pieces[g].data(), plan.pieces[g].size() * sizeof(ndx_piece));
+      off += counts[g];
+    }
+    *n_entries = plan.entries.size();
+    *n_words = plan.words;
     return 0;
   });
 }

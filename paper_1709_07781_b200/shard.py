@@ -1,0 +1,187 @@
+"""Multi-GPU WAH build: row shards, metadata exchange, boundary merge.
+
+SURVEY.md 8(e) / Appendix B.  One process per GPU (torch.distributed; NCCL on
+GPUs, gloo for the CPU tests).  Rank g builds rows [S_g, S_{g+1}) of the
+global column with global row ids (S_g a multiple of 31, so no chunk
+straddles two ranks), then:
+
+  1. ndx_wah_shard_meta: per value (value, first/last chunk, ones-fill
+     lengths at both ends of the body, body range) -- 32 B per value;
+  2. all-gather of the metadata (<= 8 x 65,536 x 32 B = 16 MB);
+  3. every rank plans the merge over the metadata (ndactor_merge_plan, host
+     C++, replicated): merged (value, offset, length) table and, per local
+     value, where its words go and which end words change;
+  4. the words are gathered to rank 0 (point-to-point over NVLink) and
+     ndx_wah_assemble copies every piece into place.
+
+The result on rank 0 is bit-identical to a single-device build of the whole
+column.  No data-path work runs on the host: step 3 touches only metadata.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import runtime as _rt
+
+META_DTYPE = np.dtype([("value", "<u4"), ("f", "<u4"), ("l", "<u4"), ("a", "<u4"), ("z", "<u4"),
+                       ("body_off", "<u4"), ("body_len", "<u4"), ("skip", "<u4")])
+PIECE_DTYPE = np.dtype([("dst", "<u8"), ("src_off", "<u4"), ("src_len", "<u4"), ("lead", "<u4"),
+                        ("pad", "<u4")])
+assert META_DTYPE.itemsize == 32 and PIECE_DTYPE.itemsize == 24
+
+
+def shard_bounds(n: int, shards: int) -> np.ndarray:
+    """S_0..S_G: inner bounds multiples of 31, chunk counts balanced."""
+    lib = _rt.load()
+    out = np.zeros(shards + 1, np.uint64)
+    _rt._check(lib.ndactor_shard_bounds(n, shards, out.ctypes.data), "shard_bounds")
+    return out
+
+
+def plan_merge(metas: list[np.ndarray]):
+    """Merge plan over per-shard metadata (each META_DTYPE, ascending values).
+
+    Returns (entries (D,3) u32, pieces list per shard (PIECE_DTYPE), words)."""
+    lib = _rt.load()
+    counts = np.array([m.size for m in metas], np.uint64)
+    cat = np.ascontiguousarray(np.concatenate(metas) if metas else np.zeros(0, META_DTYPE), META_DTYPE)
+    total = int(counts.sum())
+    entries = np.zeros((max(total, 1), 3), np.uint32)
+    pieces = np.zeros(max(total, 1), PIECE_DTYPE)
+    ne, nw = ctypes.c_uint64(), ctypes.c_uint64()
+    _rt._check(lib.ndactor_merge_plan(len(metas), cat.ctypes.data, counts.ctypes.data, entries.ctypes.data,
+                                      pieces.ctypes.data, ctypes.byref(ne), ctypes.byref(nw)), "merge_plan")
+    out, off = [], 0
+    for c in counts.tolist():
+        out.append(pieces[off:off + c].copy())
+        off += c
+    return entries[: ne.value].copy(), out, int(nw.value)
+
+
+# ---------------------------------------------------------------------------
+# Collectives (torch.distributed; tensors on the backend's device)
+
+def _dev_for(group=None):
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+
+def exchange_meta(meta: np.ndarray, group=None) -> list[np.ndarray]:
+    """All-gather every rank's metadata (variable length)."""
+    import torch
+    import torch.distributed as dist
+    dev = _dev_for(group)
+    ws = dist.get_world_size(group)
+    cnt = torch.tensor([meta.size], dtype=torch.int64, device=dev)
+    cnts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
+    dist.all_gather(cnts, cnt, group=group)
+    sizes = [int(c.item()) for c in cnts]
+    cap = max(max(sizes), 1)
+    buf = np.zeros(cap, META_DTYPE)
+    buf[: meta.size] = meta
+    t = torch.from_numpy(buf.view(np.int32).copy()).to(dev)
+    outs = [torch.zeros_like(t) for _ in range(ws)]
+    dist.all_gather(outs, t, group=group)
+    return [o.cpu().numpy().view(META_DTYPE)[:s].copy() for o, s in zip(outs, sizes)]
+
+
+def gather_words(words, dst: int = 0, group=None):
+    """Point-to-point gather of every rank's local words (a 1-D int32 tensor
+    on the backend's device) to `dst`; returns the list on dst, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    rank, ws = dist.get_rank(group), dist.get_world_size(group)
+    dev = words.device
+    n = torch.tensor([words.numel()], dtype=torch.int64, device=dev)
+    ns = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
+    dist.all_gather(ns, n, group=group)
+    if rank != dst:
+        if words.numel():
+            dist.send(words.contiguous(), dst, group=group)
+        return None
+    out = []
+    for g in range(ws):
+        k = int(ns[g].item())
+        if g == rank:
+            out.append(words)
+        else:
+            buf = torch.empty(k, dtype=words.dtype, device=dev)
+            if k:
+                dist.recv(buf, g, group=group)
+            out.append(buf)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# GPU path
+
+class ShardBuilder:
+    """Local build of one shard on this rank's GPU + its metadata."""
+
+    def __init__(self, capacity: int = 0, device: int = 0):
+        from . import ndx
+        self.ndx = ndx
+        self.b = ndx.WahBuilder(capacity, device)
+        self.torch = self.b.torch
+
+    def build(self, keys, n: int, row_base: int):
+        """keys: device int32 tensor (n values).  Returns (W, D, meta device
+        tensor) after the four stages and the metadata kernel."""
+        t, ndx = self.torch, self.ndx
+        self.b.launch(keys, n, row_base)
+        W, D = self.b.counts()
+        meta = t.empty(max(D, 1) * 8, dtype=t.int32, device=keys.device)
+        ndx.check(self.b.lib.ndx_wah_shard_meta(ndx._ptr(self.b.pairs), n, ndx._ptr(self.b.entries), D,
+                                               ndx._ptr(self.b.words), ndx._ptr(meta),
+                                               t.cuda.current_stream().cuda_stream), "shard_meta")
+        return W, D, meta
+
+    @property
+    def words(self):
+        return self.b.words
+
+
+def assemble(staged: list, pieces: list[np.ndarray], total_words: int, device):
+    """Copy every shard's pieces into the merged word array on `device`
+    (ndx_wah_assemble).  staged[g]: shard g's local words (device int32)."""
+    import torch
+    from . import ndx
+    lib = ndx.load()
+    sizes = [int(s.numel()) for s in staged]
+    base = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    src = torch.cat([s.reshape(-1) for s in staged]) if staged else torch.zeros(0, dtype=torch.int32, device=device)
+    allp = []
+    for g, p in enumerate(pieces):
+        q = p.copy()
+        q["src_off"] = (q["src_off"].astype(np.int64) + base[g]).astype(np.uint32)
+        allp.append(q)
+    cat = np.concatenate(allp) if allp else np.zeros(0, PIECE_DTYPE)
+    if base[-1] >= 2 ** 32:
+        raise ValueError("staged words exceed u32 offsets")
+    pd = torch.from_numpy(cat.view(np.uint8).copy()).to(device)
+    out = torch.empty(max(total_words, 1), dtype=torch.int32, device=device)
+    ndx.check(lib.ndx_wah_assemble(ndx._ptr(src), ndx._ptr(pd), cat.size, ndx._ptr(out),
+                                   torch.cuda.current_stream().cuda_stream), "assemble")
+    return out[:total_words]
+
+
+def build_distributed(values_local: np.ndarray, row_base: int, builder: ShardBuilder, group=None):
+    """The whole multi-GPU build for this rank's shard (one process per GPU).
+
+    Returns (entries (D,3) u32 numpy, words device tensor) on rank 0 and
+    (entries, None) elsewhere; entries are replicated on every rank."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device())
+    keys = torch.from_numpy(np.ascontiguousarray(values_local, np.uint32).view(np.int32)).to(dev)
+    n = keys.numel()
+    W, D, meta_d = builder.build(keys, n, row_base)
+    meta = meta_d[: D * 8].cpu().numpy().view(META_DTYPE)
+    metas = exchange_meta(meta, group)
+    entries, pieces, total = plan_merge(metas)
+    staged = gather_words(builder.words[:W], dst=0, group=group)
+    if dist.get_rank(group) != 0:
+        return entries, None
+    return entries, assemble(staged, pieces, total, dev)

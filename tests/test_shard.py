@@ -1,0 +1,107 @@
+"""Multi-GPU build host logic on CPU: row shards, the merge plan of SURVEY.md
+Appendix B (libndactor.so, ndactor_merge_plan) and the torch.distributed
+exchange over gloo with world_size 2.  Every merged index must equal the
+oracle's index of the whole column, bit for bit."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1709_07781_b200 import shard
+from tests import shard_helpers as H
+
+
+@pytest.mark.parametrize("n,g", [(1, 1), (30, 2), (31, 2), (100, 3), (310, 4), (10**6 + 7, 8), (2**30, 8)])
+def test_shard_bounds(n, g):
+    b = shard.shard_bounds(n, g)
+    assert b[0] == 0 and b[-1] == n and np.all(np.diff(b.astype(np.int64)) >= 0)
+    assert all(int(x) % 31 == 0 for x in b[:-1])
+    sizes = np.diff(b.astype(np.int64))
+    if n >= 31 * g:
+        assert sizes.max() - sizes.min() <= 31
+
+
+def _merged(port, v, g):
+    b = shard.shard_bounds(v.size, g).astype(np.int64)
+    metas, words = [], []
+    for k in range(g):
+        part = v[b[k]:b[k + 1]]
+        if part.size == 0:
+            metas.append(np.zeros(0, shard.META_DTYPE))
+            words.append(np.zeros(0, np.uint32))
+            continue
+        e, w = H.local_index(port, part, int(b[k]))
+        metas.append(H.local_meta(part, int(b[k]), e, w))
+        words.append(w)
+    entries, pieces, total = shard.plan_merge(metas)
+    return entries, H.assemble(words, pieces, total)
+
+
+@pytest.mark.parametrize("g", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("name", sorted(H.columns()))
+def test_merge_plan_matches_whole_column(port, name, g):
+    v = H.columns()[name]
+    entries, words = _merged(port, v, g)
+    ref = port.reference_index(v)
+    assert np.array_equal(entries, ref.entries), (name, g)
+    assert np.array_equal(words, ref.words), (name, g)
+
+
+def test_merge_plan_fuses_ones_over_cuts(port):
+    entries, words = _merged(port, np.full(93, 7, np.uint32), 3)
+    assert words.tolist() == [0xC0000003] and entries.tolist() == [[7, 0, 1]]
+
+
+def test_merge_plan_rejects_unsorted():
+    m = np.zeros(2, shard.META_DTYPE)
+    m["value"] = [5, 3]
+    m["body_len"] = 1
+    with pytest.raises(Exception):
+        shard.plan_merge([m])
+
+
+def _worker(rank, ws, port_num, q):
+    try:
+        import torch.distributed as dist
+        import torch
+        import oracle
+
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port_num)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        port = oracle.Port()
+        v = H.columns()["hot_cold"]
+        b = shard.shard_bounds(v.size, ws).astype(np.int64)
+        part = v[b[rank]:b[rank + 1]]
+        e, w = H.local_index(port, part, int(b[rank]))
+        metas = shard.exchange_meta(H.local_meta(part, int(b[rank]), e, w))
+        entries, pieces, total = shard.plan_merge(metas)
+        staged = shard.gather_words(torch.from_numpy(w.view(np.int32).copy()))
+        if rank == 0:
+            merged = H.assemble([s.numpy().view(np.uint32) for s in staged], pieces, total)
+            ref = port.reference_index(v)
+            q.put(bool(np.array_equal(merged, ref.words) and np.array_equal(entries, ref.entries)))
+        else:
+            q.put(bool(len(entries) > 0))
+        dist.destroy_process_group()
+    except Exception as ex:  # pragma: no cover - reported through the queue
+        q.put(repr(ex))
+
+
+def test_distributed_exchange_gloo_world2():
+    import socket
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port_num = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_num, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [True, True], res
