@@ -112,11 +112,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or getattr(args, "force_sharded", False):
+        import torch
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo", rank=rank, world_size=world)
     return world, rank, local
 
 
@@ -178,6 +182,114 @@ def run_reference(args, cfg):
     return 0
 
 
+def run_sharded(args, cfg, world, rank, local):
+    """N > 1: one process per GPU.  The global column is the concatenation of
+    the ranks' shards (31-aligned bounds over world*n values, each shard
+    generated from seed 42+rank); a step is the local build with global row
+    ids + shard metadata + NCCL all-gather of the metadata + the merge plan +
+    each rank writing its pieces into final form in the merged word array.
+    The gather of all words to rank 0 is timed once, separately."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_07781_b200 import shard
+
+    dev = torch.device("cuda", local)
+    n = args.n or cfg["n"]
+    bounds = shard.shard_bounds(world * n, world).astype(np.int64)
+    base, n_r = int(bounds[rank]), int(bounds[rank + 1] - bounds[rank])
+    host_keys = torch.empty(n_r, dtype=torch.int32, pin_memory=True)
+    gen_values(cfg, n_r, rank, host_keys.numpy().view(np.uint32))
+    keys = host_keys.to(dev)
+    sb = shard.ShardBuilder(n_r, device=local)
+    stream = torch.cuda.current_stream()
+    state = {}
+
+    def step(k):
+        W, D, meta_d = sb.build(k, n_r, base)
+        meta = meta_d[: D * 8].cpu().numpy().view(shard.META_DTYPE)
+        metas = shard.exchange_meta(meta)
+        entries, pieces, total = shard.plan_merge(metas)
+        if state.get("cap", 0) < total:
+            state["out"] = torch.empty(total, dtype=torch.int32, device=dev)
+            state["cap"] = total
+        shard.assemble([sb.words[:W]], [pieces[rank]], total, dev, out=state["out"])
+        state.update(W=W, D=D, entries=entries, pieces=pieces, total=total)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    W_ = max(args.warmup, 3)
+    K = args.steps
+    for _ in range(W_):
+        step(keys)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(K):
+        step(keys)
+    a1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(a0.elapsed_time(a1) / K)
+    total_values = world * n
+    value = total_values / (ms * 1e-3)
+
+    # the gathered index on rank 0 (words over NVLink, then all pieces placed)
+    barrier()
+    g0 = time.perf_counter()
+    staged = shard.gather_words(sb.words[: state["W"]], dst=0)
+    if rank == 0:
+        shard.assemble(staged, state["pieces"], state["total"], dev, out=state["out"])
+    barrier()
+    gather_ms = max_over_ranks((time.perf_counter() - g0) * 1e3)
+
+    # end to end: pinned host keys in, every step; the rank's merged table and
+    # its own words back to the host
+    e2e_steps = max(1, min(K, args.e2e_steps))
+    hw = torch.empty(max(state["W"], 1), dtype=torch.int32, pin_memory=True)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        kk = host_keys.to(dev, non_blocking=True)
+        step(kk)
+        hw[: state["W"]].copy_(sb.words[: state["W"]], non_blocking=True)
+        torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W_, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "values_per_gpu": n, "keys": cfg["k"],
+                   "distribution": "zipf s=1" if cfg["kind"] == "zipf" else "uniform",
+                   "l2": "inputs larger than L2 (4 B keys x values per GPU > 126 MB)",
+                   "parallelism": f"row shards x{world} (31-aligned), NCCL metadata all-gather, "
+                                  f"boundary merge (SURVEY App. B)",
+                   "words": state["total"], "distinct": int(len(state["entries"])),
+                   "path": "per-rank 4-stage build + shard meta + all-gather + merge plan + own pieces "
+                           "into final form; gather to rank 0 timed separately"},
+        "gather_to_rank0_ms": gather_ms,
+        "e2e": {"value": total_values / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
+                "d2h_bytes_per_step": 4 * state["W"], "ms_per_step": e2e_ms},
+        "gpu_launches": 13 * K,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -186,6 +298,8 @@ def run_ours(args, cfg):
 
     world, rank, local = dist_setup(args)
     torch.cuda.set_device(local)
+    if world > 1 or args.force_sharded:
+        return run_sharded(args, cfg, world, rank, local)
     dev = torch.device("cuda", local)
     n = args.n or cfg["n"]
 
@@ -340,6 +454,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the multi-GPU step (shard meta, all-gather, merge) even at N=1")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

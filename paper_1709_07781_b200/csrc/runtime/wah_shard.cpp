@@ -45,6 +45,7 @@ MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
   plan.entries.reserve(total);
   std::vector<std::size_t> head(G, 0);
   std::vector<std::pair<std::size_t, std::size_t>> group;
+  std::vector<std::pair<ndx_piece*, std::uint64_t>> placed;
   std::uint64_t out = 0;
   for (;;) {
     // next value: the smallest head over the shards (G is small)
@@ -63,8 +64,7 @@ MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
     std::uint64_t len = 0;
     LastWord last;
     std::uint32_t prev_l = 0;
-    std::vector<std::pair<ndx_piece*, std::uint64_t>> placed;
-    placed.reserve(group.size());
+    placed.clear();
     for (std::size_t k = 0; k < group.size(); ++k) {
       const ndx_shard_meta& m = shards[group[k].first][group[k].second];
       ndx_piece& p = plan.pieces[group[k].first][group[k].second];

@@ -143,25 +143,54 @@ class ShardBuilder:
         return self.b.words
 
 
-def assemble(staged: list, pieces: list[np.ndarray], total_words: int, device):
+def split_pieces(p: np.ndarray, block: int = 4096) -> np.ndarray:
+    """Cut pieces into runs of at most `block` words so the copy spreads over
+    the whole GPU (a hot value's piece can hold tens of millions of words)."""
+    if p.size == 0:
+        return p
+    body = p["src_len"].astype(np.int64)
+    nb = np.maximum(1, (body + block - 1) // block)
+    if int(nb.max()) == 1:
+        return p
+    idx = np.repeat(np.arange(p.size), nb)
+    first = np.concatenate([[0], np.cumsum(nb)[:-1]])
+    k = np.arange(idx.size) - np.repeat(first, nb)  # block index inside its piece
+    out = np.zeros(idx.size, PIECE_DTYPE)
+    lead = p["lead"][idx]
+    has_lead = (lead != 0).astype(np.int64)
+    out["src_off"] = (p["src_off"][idx].astype(np.int64) + k * block).astype(np.uint32)
+    out["src_len"] = np.minimum(block, body[idx] - k * block).astype(np.uint32)
+    out["lead"] = np.where(k == 0, lead, 0)
+    out["dst"] = (p["dst"][idx].astype(np.int64) + np.where(k == 0, 0, has_lead + k * block)).astype(np.uint64)
+    return out
+
+
+def assemble(staged: list, pieces: list[np.ndarray], total_words: int, device, out=None):
     """Copy every shard's pieces into the merged word array on `device`
-    (ndx_wah_assemble).  staged[g]: shard g's local words (device int32)."""
+    (ndx_wah_assemble).  staged[g]: shard g's local words (device int32).
+    With only some shards' pieces, only their positions of `out` are written
+    (a rank putting its own pieces into final form)."""
     import torch
     from . import ndx
     lib = ndx.load()
     sizes = [int(s.numel()) for s in staged]
     base = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    src = torch.cat([s.reshape(-1) for s in staged]) if staged else torch.zeros(0, dtype=torch.int32, device=device)
+    if len(staged) == 1:
+        src = staged[0].reshape(-1)
+    else:
+        src = torch.cat([s.reshape(-1) for s in staged]) if staged else torch.zeros(0, dtype=torch.int32,
+                                                                                   device=device)
     allp = []
     for g, p in enumerate(pieces):
         q = p.copy()
         q["src_off"] = (q["src_off"].astype(np.int64) + base[g]).astype(np.uint32)
         allp.append(q)
-    cat = np.concatenate(allp) if allp else np.zeros(0, PIECE_DTYPE)
+    cat = split_pieces(np.concatenate(allp) if allp else np.zeros(0, PIECE_DTYPE))
     if base[-1] >= 2 ** 32:
         raise ValueError("staged words exceed u32 offsets")
     pd = torch.from_numpy(cat.view(np.uint8).copy()).to(device)
-    out = torch.empty(max(total_words, 1), dtype=torch.int32, device=device)
+    if out is None:
+        out = torch.empty(max(total_words, 1), dtype=torch.int32, device=device)
     ndx.check(lib.ndx_wah_assemble(ndx._ptr(src), ndx._ptr(pd), cat.size, ndx._ptr(out),
                                    torch.cuda.current_stream().cuda_stream), "assemble")
     return out[:total_words]

@@ -105,3 +105,19 @@ def test_distributed_exchange_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == [True, True], res
+
+
+@pytest.mark.parametrize("block", [1, 2, 3, 64])
+def test_split_pieces_same_result(port, block):
+    v = H.columns()["ones_across"]
+    v = np.concatenate([v, H.columns()["hot_cold"]])
+    b = shard.shard_bounds(v.size, 3).astype(np.int64)
+    metas, words = [], []
+    for k in range(3):
+        part = v[b[k]:b[k + 1]]
+        e, w = H.local_index(port, part, int(b[k]))
+        metas.append(H.local_meta(part, int(b[k]), e, w))
+        words.append(w)
+    entries, pieces, total = shard.plan_merge(metas)
+    split = [shard.split_pieces(p, block) for p in pieces]
+    assert np.array_equal(H.assemble(words, split, total), H.assemble(words, pieces, total))

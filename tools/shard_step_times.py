@@ -1,0 +1,39 @@
+"""Time the pieces of one sharded step on one GPU (world size 1)."""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_1709_07781_b200 import gen, shard  # noqa: E402
+
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+os.environ.setdefault("MASTER_PORT", "29544")
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1)
+n = 1 << 28
+v = gen.zipf(42, n, 65536, 1.0)
+keys = torch.from_numpy(v.view(np.int32)).cuda()
+sb = shard.ShardBuilder(n)
+out = None
+for it in range(4):
+    t = [time.perf_counter()]
+    W, D, meta_d = sb.build(keys, n, 0)
+    torch.cuda.synchronize(); t.append(time.perf_counter())
+    meta = meta_d[: D * 8].cpu().numpy().view(shard.META_DTYPE)
+    t.append(time.perf_counter())
+    metas = shard.exchange_meta(meta)
+    t.append(time.perf_counter())
+    entries, pieces, total = shard.plan_merge(metas)
+    t.append(time.perf_counter())
+    if out is None:
+        out = torch.empty(total, dtype=torch.int32, device="cuda")
+    shard.assemble([sb.words[:W]], [pieces[0]], total, torch.device("cuda"), out=out)
+    torch.cuda.synchronize(); t.append(time.perf_counter())
+    print("build %.2f meta_d2h %.2f exchange %.2f plan %.2f assemble %.2f ms" %
+          tuple((b - a) * 1e3 for a, b in zip(t, t[1:])))
+dist.destroy_process_group()
