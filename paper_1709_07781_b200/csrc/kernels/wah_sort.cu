@@ -33,20 +33,45 @@
 
 namespace ndx {
 
-#ifndef NDX_SORT_THREADS
-#define NDX_SORT_THREADS 256
+// Tile shape of the scatter passes (measured on B200, tools/var_run.sh):
+// bigger tiles amortise the per-tile look-back over more pairs, so the
+// byte passes run 256 threads x 32 pairs (8192-pair tiles, 2 CTAs/SM) and
+// the wide pass -- whose look-back covers up to 2048 digits per tile --
+// 512 threads x 32 pairs (16384-pair tiles, 1 CTA/SM).
+#ifndef NDX_SORT_THREADS_B
+#define NDX_SORT_THREADS_B 256
 #endif
-#ifndef NDX_SORT_IPT
-#define NDX_SORT_IPT 16
+#ifndef NDX_SORT_IPT_B
+#define NDX_SORT_IPT_B 32
 #endif
-#ifndef NDX_SORT_MINB
-#define NDX_SORT_MINB 3
+#ifndef NDX_SORT_MINB_B
+#define NDX_SORT_MINB_B 2
 #endif
-constexpr int kSortThreads = NDX_SORT_THREADS;
-constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortIPT = NDX_SORT_IPT;                // items per thread
-constexpr int kSortWarpItems = 32 * kSortIPT;         // 512
-constexpr int kSortTile = kSortThreads * kSortIPT;    // 4096 pairs
+#ifndef NDX_SORT_THREADS_W
+#define NDX_SORT_THREADS_W 512
+#endif
+#ifndef NDX_SORT_IPT_W
+#define NDX_SORT_IPT_W 32
+#endif
+#ifndef NDX_SORT_MINB_W
+#define NDX_SORT_MINB_W 1
+#endif
+#ifndef NDX_SORT_ATOMRANK
+#define NDX_SORT_ATOMRANK 0
+#endif
+#ifndef NDX_SORT_MATCH_TREE
+#define NDX_SORT_MATCH_TREE 0
+#endif
+template <int MAXB>
+struct Shape {
+  static constexpr bool kWide = MAXB > 8;
+  static constexpr int THREADS = kWide ? NDX_SORT_THREADS_W : NDX_SORT_THREADS_B;
+  static constexpr int IPT = kWide ? NDX_SORT_IPT_W : NDX_SORT_IPT_B;  // pairs per thread
+  static constexpr int MINB = kWide ? NDX_SORT_MINB_W : NDX_SORT_MINB_B;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int WARP_ITEMS = 32 * IPT;
+  static constexpr int TILE = THREADS * IPT;
+};
 
 // ------------------------------------------------------------------ S1 ----
 
@@ -287,16 +312,39 @@ __device__ __forceinline__ bool pass_info(const SortArgs& a, int which, PassInfo
 template <int MAXB>
 struct SortSmem {
   static constexpr int NB = 1 << MAXB;
-  static constexpr size_t kHBytes = size_t(kSortWarps) * NB * sizeof(uint16_t);
-  static constexpr size_t kSBytes = size_t(kSortTile) * sizeof(uint64_t);
+  using SH = Shape<MAXB>;
+  static constexpr size_t kHBytes = size_t(SH::WARPS) * NB * sizeof(uint16_t);
+  static constexpr size_t kSBytes = size_t(SH::TILE) * sizeof(uint64_t);
   static constexpr size_t kUnion = kHBytes > kSBytes ? kHBytes : kSBytes;
   static constexpr size_t kBytes = kUnion + 2 * NB * sizeof(uint32_t) + 16;
 };
 
 // Lanes of the warp whose `BITS`-wide digit equals mine: per bit one
-// predicate, one ballot, one select, one 3-input logic op.
+// ballot and one select of it or its complement, then a 3-input AND tree
+// (depth 2-3 instead of a chain of BITS dependent ANDs).
 template <int BITS>
 __device__ __forceinline__ unsigned warp_match(uint32_t d) {
+#if NDX_SORT_MATCH_TREE
+  unsigned e[BITS];
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool p = (d >> b) & 1u;
+    const unsigned v = __ballot_sync(kFull, p);
+    e[b] = p ? v : ~v;
+  }
+  unsigned acc[(BITS + 2) / 3];
+#pragma unroll
+  for (int i = 0; i < (BITS + 2) / 3; ++i) {
+    unsigned x = e[3 * i];
+    if (3 * i + 1 < BITS) x &= e[3 * i + 1];
+    if (3 * i + 2 < BITS) x &= e[3 * i + 2];
+    acc[i] = x;
+  }
+  unsigned peers = acc[0];
+#pragma unroll
+  for (int i = 1; i < (BITS + 2) / 3; ++i) peers &= acc[i];
+  return peers;
+#else
   unsigned peers = kFull;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
@@ -311,6 +359,7 @@ __device__ __forceinline__ unsigned warp_match(uint32_t d) {
         : "r"(d), "r"(1u << b));
   }
   return peers;
+#endif
 }
 
 struct TileCtx {
@@ -365,22 +414,22 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* st, uint64_t tile, 
 // time, so the ballot match unrolls straight); FULL tiles skip every bounds
 // check.  Element order within a warp is round-major / lane-minor, which is
 // row order, so ranks taken round by round are stable.
-template <int BITS, int NBMAX, bool FULL>
+template <class SH, int BITS, int NBMAX, bool FULL>
 __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint32_t tile_n) {
   constexpr uint32_t NB = 1u << BITS;
   constexpr uint32_t DMASK = NB - 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t tile_start = tile * kSortTile;
+  const uint64_t tile_start = tile * SH::TILE;
   uint16_t* Hw = t.H + warp * NBMAX;
   for (uint32_t d = lane; d < NB; d += 32) Hw[d] = 0;
-  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads) t.cnt[d] = 0;
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) t.cnt[d] = 0;
 
-  const uint32_t wofs = uint32_t(warp) * kSortWarpItems + lane;
-  uint32_t key[kSortIPT], pay[kSortIPT];
+  const uint32_t wofs = uint32_t(warp) * SH::WARP_ITEMS + lane;
+  uint32_t key[SH::IPT], pay[SH::IPT];
   if (t.in_pairs) {
     const uint64_t* pp = t.in_pairs + tile_start + wofs;
 #pragma unroll
-    for (int r = 0; r < kSortIPT; ++r) {
+    for (int r = 0; r < SH::IPT; ++r) {
       const uint64_t e = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(pp + r * 32) : 0ull;
       key[r] = uint32_t(e);
       pay[r] = uint32_t(e >> 32);
@@ -388,34 +437,34 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   } else {
     const uint32_t* kp = t.in_keys + tile_start + wofs;
 #pragma unroll
-    for (int r = 0; r < kSortIPT; ++r)
+    for (int r = 0; r < SH::IPT; ++r)
       key[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(kp + r * 32) : 0u;
     if (t.in_pays) {
       const uint32_t* rp = t.in_pays + tile_start + wofs;
 #pragma unroll
-      for (int r = 0; r < kSortIPT; ++r)
+      for (int r = 0; r < SH::IPT; ++r)
         pay[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(rp + r * 32) : 0u;
     } else {
       const uint32_t r0 = t.row_base + uint32_t(tile_start) + wofs;
 #pragma unroll
-      for (int r = 0; r < kSortIPT; ++r) pay[r] = r0 + r * 32;
+      for (int r = 0; r < SH::IPT; ++r) pay[r] = r0 + r * 32;
     }
   }
   __syncthreads();
 
   // ---- early counts: tile histogram, published before the heavy ranking
 #pragma unroll
-  for (int r = 0; r < kSortIPT; ++r)
+  for (int r = 0; r < SH::IPT; ++r)
     if (FULL || wofs + r * 32 < tile_n) atomicAdd(&t.cnt[((key[r] - t.base) >> t.shift) & DMASK], 1u);
   __syncthreads();
   uint64_t* st = t.status + tile * NB;
-  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads)
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS)
     st_relaxed_u64(&st[d], st_word(t.epoch, tile == 0 ? kStPrefix : kStAgg, t.cnt[d]));
 
   // ---- rank
-  uint32_t rank[kSortIPT];
+  uint32_t rank[SH::IPT];
 #pragma unroll
-  for (int r = 0; r < kSortIPT; ++r) {
+  for (int r = 0; r < SH::IPT; ++r) {
     const uint32_t d = ((key[r] - t.base) >> t.shift) & DMASK;
     unsigned peers = warp_match<BITS>(d);
     bool valid = true;
@@ -424,20 +473,35 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       peers &= __ballot_sync(kFull, valid);
     }
     const int leader = valid ? __ffs(peers) - 1 : lane;
+#if NDX_SORT_ATOMRANK
+    // one shared atomic per digit group: the counters are u16 pairs packed
+    // in u32 words (a warp counts at most 32*IPT < 2^16 per digit), and a
+    // warp's atomics to one word apply in program order, so round r+1 sees
+    // round r without a load/store chain between rounds
+    uint32_t old = 0;
+    if (valid && lane == leader) {
+      const uint32_t sh = (d & 1u) * 16u;
+      old = (atomicAdd(reinterpret_cast<uint32_t*>(Hw) + (d >> 1), uint32_t(__popc(peers)) << sh) >> sh) &
+            0xffffu;
+    }
+    old = __shfl_sync(kFull, old, leader);
+    rank[r] = old + __popc(peers & lanemask_lt());
+#else
     uint32_t old = 0;
     if (lane == leader) old = Hw[d];
     old = __shfl_sync(kFull, old, leader);
     if (valid && lane == leader) Hw[d] = uint16_t(old + __popc(peers));
     rank[r] = old + __popc(peers & lanemask_lt());
     __syncwarp();
+#endif
   }
   __syncthreads();
 
   // ---- per digit: warp offsets (in place); tile-local digit starts
-  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads) {
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
     uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) {
+    for (int w = 0; w < SH::WARPS; ++w) {
       const uint32_t c = t.H[w * NBMAX + d];
       t.H[w * NBMAX + d] = uint16_t(sum);
       sum += c;
@@ -446,7 +510,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   block_excl_scan(t.cnt, t.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
 
   // ---- look-back: global base of each digit for this tile
-  for (uint32_t d = threadIdx.x; d < NB; d += kSortThreads) {
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
     const uint32_t c = t.cnt[d], local = t.gbase[d];
     uint64_t excl = 0;
     if (tile > 0) {
@@ -456,25 +520,25 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       st_relaxed_u64(&st[d], st_word(t.epoch, kStPrefix, excl + c));
     }
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) t.H[w * NBMAX + d] += uint16_t(local);
+    for (int w = 0; w < SH::WARPS; ++w) t.H[w * NBMAX + d] += uint16_t(local);
     t.gbase[d] = t.bstart[d] + uint32_t(excl) - local;
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kSortIPT; ++r) {
+  for (int r = 0; r < SH::IPT; ++r) {
     const uint32_t d = ((key[r] - t.base) >> t.shift) & DMASK;
     rank[r] += Hw[d];
   }
   __syncthreads();  // H no longer read: S may overwrite it
 #pragma unroll
-  for (int r = 0; r < kSortIPT; ++r)
+  for (int r = 0; r < SH::IPT; ++r)
     if (FULL || wofs + r * 32 < tile_n) t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
   __syncthreads();
 
   // ---- scatter: consecutive local slots of one digit are consecutive globally
-  const uint32_t lim = FULL ? uint32_t(kSortTile) : tile_n;
+  const uint32_t lim = FULL ? uint32_t(SH::TILE) : tile_n;
   if (t.out_keys) {
-    for (uint32_t j = threadIdx.x; j < lim; j += kSortThreads) {
+    for (uint32_t j = threadIdx.x; j < lim; j += SH::THREADS) {
       const uint64_t e = t.S[j];
       const uint32_t pos = t.gbase[((uint32_t(e) - t.base) >> t.shift) & DMASK] + j;
       t.out_keys[pos] = uint32_t(e);
@@ -482,7 +546,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     }
   } else {
 #pragma unroll 4
-    for (uint32_t j = threadIdx.x; j < lim; j += kSortThreads) {
+    for (uint32_t j = threadIdx.x; j < lim; j += SH::THREADS) {
       const uint64_t e = t.S[j];
       const uint32_t pos = t.gbase[((uint32_t(e) - t.base) >> t.shift) & DMASK] + j;
       t.out_pairs[pos] = e;
@@ -491,27 +555,27 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   __syncthreads();
 }
 
-template <int BITS, int NBMAX>
+template <class SH, int BITS, int NBMAX>
 __device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint32_t* s_tile,
                                           uint64_t n) {
-  const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
+  const uint64_t tiles = (n + SH::TILE - 1) / SH::TILE;
   for (;;) {
     if (threadIdx.x == 0) *s_tile = atomicAdd(ctr, 1u);
     __syncthreads();
     const uint64_t tile = *s_tile;
     if (tile >= tiles) return;
-    const uint32_t tn = uint32_t(umin<uint64_t>(kSortTile, n - tile * kSortTile));
-    if (tn == uint32_t(kSortTile))
-      tile_pass<BITS, NBMAX, true>(t, tile, tn);
+    const uint32_t tn = uint32_t(umin<uint64_t>(SH::TILE, n - tile * SH::TILE));
+    if (tn == uint32_t(SH::TILE))
+      tile_pass<SH, BITS, NBMAX, true>(t, tile, tn);
     else
-      tile_pass<BITS, NBMAX, false>(t, tile, tn);
+      tile_pass<SH, BITS, NBMAX, false>(t, tile, tn);
   }
 }
 
 // One stable scatter pass over persistent CTAs.  Pass q writes X iff
 // (P-1-q) is even, so the last pass lands in X.
 template <int MAXB>
-__global__ __launch_bounds__(kSortThreads, NDX_SORT_MINB) void k_pass(SortArgs a, int which) {
+__global__ __launch_bounds__(Shape<MAXB>::THREADS, Shape<MAXB>::MINB) void k_pass(SortArgs a, int which) {
   if (which < 0 && blockIdx.x == 0 && threadIdx.x == 0)
     a.ctl->row_hi = a.row_base + uint32_t(a.n - 1);  // read by the emit stage
   PassInfo pi;
@@ -539,19 +603,19 @@ __global__ __launch_bounds__(kSortThreads, NDX_SORT_MINB) void k_pass(SortArgs a
   uint32_t* s_tile = t.gbase + SM::NB;
   uint32_t* ctr = &a.ctl->tile_ctr[which + 2];  // [0] emit, [1] wide, [2..5] bytes
   if (MAXB == 8) {
-    tile_loop<8, SM::NB>(t, ctr, s_tile, a.n);
+    tile_loop<Shape<MAXB>, 8, SM::NB>(t, ctr, s_tile, a.n);
   } else {
     // digits above `bits` are zero for every key, so a wider match is exact
     if (pi.bits <= 4)
-      tile_loop<4, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB>, 4, SM::NB>(t, ctr, s_tile, a.n);
     else if (pi.bits <= 8)
-      tile_loop<8, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB>, 8, SM::NB>(t, ctr, s_tile, a.n);
     else if (pi.bits <= 9)
-      tile_loop<9, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB>, 9, SM::NB>(t, ctr, s_tile, a.n);
     else if (pi.bits <= 10)
-      tile_loop<10, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB>, 10, SM::NB>(t, ctr, s_tile, a.n);
     else
-      tile_loop<(MAXB > 10 ? 11 : 10), SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB>, (MAXB > 10 ? 11 : 10), SM::NB>(t, ctr, s_tile, a.n);
   }
 }
 
@@ -578,11 +642,11 @@ static int launch_cfg(LaunchCfg** out) {
     if ((e = cudaFuncSetAttribute(k_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sb))))
       return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_wide, k_pass<kWideMaxBits>,
-                                                           kSortThreads, sw)))
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+             &c.occ_wide, k_pass<kWideMaxBits>, Shape<kWideMaxBits>::THREADS, sw)))
       return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_pass<8>, kSortThreads,
-                                                           sb)))
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_pass<8>,
+                                                           Shape<8>::THREADS, sb)))
       return e;
 #ifdef NDX_SORT_OCC_CAP
     c.occ_wide = umin(c.occ_wide, NDX_SORT_OCC_CAP);
@@ -596,14 +660,18 @@ static int launch_cfg(LaunchCfg** out) {
   return 0;
 }
 
-static uint64_t sort_tiles(uint64_t n) { return (n + kSortTile - 1) / kSortTile; }
+template <int MAXB>
+static uint64_t sort_tiles(uint64_t n) {
+  return (n + Shape<MAXB>::TILE - 1) / Shape<MAXB>::TILE;
+}
 
 static int launch_sort(SortArgs a, cudaStream_t s, LaunchCfg* c) {
-  const uint64_t tiles = sort_tiles(a.n);
-  const int gw = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_wide));
-  const int gb = int(umin<uint64_t>(tiles, uint64_t(c->sms) * c->occ_byte));
-  k_pass<kWideMaxBits><<<gw, kSortThreads, SortSmem<kWideMaxBits>::kBytes, s>>>(a, -1);
-  for (int k = 0; k < 4; ++k) k_pass<8><<<gb, kSortThreads, SortSmem<8>::kBytes, s>>>(a, k);
+  const int gw = int(umin<uint64_t>(sort_tiles<kWideMaxBits>(a.n), uint64_t(c->sms) * c->occ_wide));
+  const int gb = int(umin<uint64_t>(sort_tiles<8>(a.n), uint64_t(c->sms) * c->occ_byte));
+  k_pass<kWideMaxBits>
+      <<<gw, Shape<kWideMaxBits>::THREADS, SortSmem<kWideMaxBits>::kBytes, s>>>(a, -1);
+  for (int k = 0; k < 4; ++k)
+    k_pass<8><<<gb, Shape<8>::THREADS, SortSmem<8>::kBytes, s>>>(a, k);
   return cudaGetLastError();
 }
 
@@ -619,9 +687,11 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, uint32_t* epo
   return cudaGetLastError();
 }
 
-// Status buffer: [256 B header: u32 epoch counter][tiles x 2048 statuses]
+// Status buffer: [256 B header: u32 epoch counter][statuses of the pass with
+// the most: wide tiles x 2048 digits or byte tiles x 256 digits]
 static size_t status_bytes(uint64_t n) {
-  return 256 + size_t(sort_tiles(n)) * kWideBuckets * sizeof(uint64_t);
+  const uint64_t w = sort_tiles<kWideMaxBits>(n) * kWideBuckets, b = sort_tiles<8>(n) * 256;
+  return 256 + size_t(umax(w, b)) * sizeof(uint64_t);
 }
 
 }  // namespace ndx
