@@ -208,9 +208,10 @@ int ndactor_dispatch_probe_ex(ndactor_runtime* rt, uint64_t iters, double* out /
     dev.await_all();
 
     // (a) raw: back-to-back launches on the runtime stream, one sync
+    void* stream = dev.stream();
     auto t0 = clk::now();
     for (uint64_t i = 0; i < iters; ++i) {
-      int rc = ndx_tiny_increment(static_cast<uint32_t*>(counter.data()), dev.stream());
+      int rc = ndx_tiny_increment(static_cast<uint32_t*>(counter.data()), stream);
       if (rc) throw std::runtime_error(ndx_error_string(rc));
     }
     out[1] = ms_since(t0);  // host enqueue time alone

@@ -22,7 +22,10 @@ namespace {
 std::string cuda_msg(int rc) { return ndx_error_string(rc); }
 }  // namespace
 
-void DeviceImpl::start() { completer = std::thread([this] { completer_loop(); }); }
+void DeviceImpl::start() {
+  completer = std::thread([this] { completer_loop(); });
+  launcher = std::thread([this] { launcher_loop(); });
+}
 
 void DeviceImpl::stop() {
   {
@@ -31,6 +34,82 @@ void DeviceImpl::stop() {
   }
   watch_cv.notify_all();
   if (completer.joinable()) completer.join();
+  {
+    std::lock_guard<std::mutex> l(q_mu);
+    q_stop = true;
+  }
+  q_cv.notify_all();
+  if (launcher.joinable()) launcher.join();
+}
+
+namespace {
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#endif
+}
+}  // namespace
+
+void DeviceImpl::push_launch(LaunchJob&& j) {
+  bool wake;
+  {
+    std::lock_guard<std::mutex> l(q_mu);
+    q.push_back(std::move(j));
+    wake = q_sleeping;
+  }
+  q_pushed.fetch_add(1, std::memory_order_release);
+  if (wake) q_cv.notify_one();
+}
+
+void DeviceImpl::drain() {
+  const std::uint64_t target = q_pushed.load(std::memory_order_acquire);
+  for (unsigned i = 0; q_done.load(std::memory_order_acquire) < target; ++i) {
+    if (i < 4096)
+      cpu_relax();
+    else
+      std::this_thread::yield();
+  }
+}
+
+void DeviceImpl::launcher_loop() {
+  std::deque<LaunchJob> batch;
+  for (;;) {
+    {
+      std::unique_lock<std::mutex> l(q_mu);
+      if (q.empty()) {
+        // a chain of requests arrives every ~microsecond: spin briefly
+        // before sleeping so a steady stream never pays a wake-up
+        l.unlock();
+        for (int i = 0; i < 20000 && q_pushed.load(std::memory_order_acquire) ==
+                                         q_done.load(std::memory_order_relaxed);
+             ++i)
+          cpu_relax();
+        l.lock();
+        if (q.empty()) {
+          q_sleeping = true;
+          q_cv.wait(l, [&] { return q_stop || !q.empty(); });
+          q_sleeping = false;
+        }
+        if (q.empty()) return;  // stopping
+      }
+      batch.swap(q);
+    }
+    for (LaunchJob& j : batch) {
+      {
+        auto& es = *j.ev;
+        if (!es.exec_started.exchange(true)) {
+          std::lock_guard<std::mutex> l(es.mu);
+          es.exec_start_tp = Clock::now();
+        }
+      }
+      j.p.stream = stream;
+      const int rc = j.launch(j.p);
+      if (rc != 0) finish_event(j.ev, false, "kernel " + j.name + ": " + ndx_error_string(rc));
+      launched.store(j.seq, std::memory_order_release);
+      q_done.fetch_add(1, std::memory_order_release);
+    }
+    batch.clear();
+  }
 }
 
 void DeviceImpl::watch(const std::shared_ptr<Event::State>& st) {
@@ -79,6 +158,7 @@ bool DeviceImpl::sync_now() {
     if (broken) {
       rc = -1;
     } else {
+      drain();
       s = issued;
       rc = ndx_event_create(&ev, 0);
       if (!rc) rc = ndx_event_record(ev, stream);
@@ -109,7 +189,7 @@ void DeviceImpl::poll() {
   {
     std::lock_guard<std::mutex> l(issue_mu);
     if (broken) return;
-    s = issued;
+    s = launched.load(std::memory_order_acquire);  // queued launches are not on the stream yet
     rc = ndx_stream_query(stream);
   }
   if (rc == 0) {
@@ -178,6 +258,7 @@ void DeviceImpl::block_put(void* p, std::size_t cls) {
   block_cache.emplace(cls, p);
   cached_bytes += cls;
   while (cached_bytes > kCacheLimit && !block_cache.empty()) {
+    drain();
     auto it = std::prev(block_cache.end());  // drop the largest
     ndx_free_async(it->second, stream);
     cached_bytes -= it->first;
@@ -186,6 +267,7 @@ void DeviceImpl::block_put(void* p, std::size_t cls) {
 }
 
 void DeviceImpl::block_trim() {
+  drain();
   for (auto& kv : block_cache) ndx_free_async(kv.second, stream);
   block_cache.clear();
   cached_bytes = 0;
@@ -220,6 +302,7 @@ void issue_now(const std::shared_ptr<DeviceImpl>& d, const Event& ev, Issue& w) 
     detail::finish_event(ev.shared_state(), false, d->broken_why);
     return;
   }
+  d->drain();
   for (const Event& dep : w.other_device) {
     auto od = dep.shared_state()->dev.lock();
     if (!od) continue;
@@ -238,6 +321,7 @@ void issue_now(const std::shared_ptr<DeviceImpl>& d, const Event& ev, Issue& w) 
   }
   auto& es = *ev.shared_state();
   es.seq.store(++d->issued, std::memory_order_release);
+  d->launched.store(d->issued, std::memory_order_release);
   bool waited;
   {
     std::lock_guard<std::mutex> lk(es.mu);
@@ -345,7 +429,11 @@ Device::~Device() {
   ndx_stream_destroy(impl_->stream);
 }
 
-void* Device::stream() const { return impl_->stream; }
+void* Device::stream() const {
+  std::lock_guard<std::mutex> l(impl_->issue_mu);
+  impl_->drain();  // everything enqueued so far is on the stream
+  return impl_->stream;
+}
 
 namespace {
 Buffer make_buffer(Device* self, const std::shared_ptr<DeviceImpl>& d, ElemType type,
@@ -363,6 +451,7 @@ Buffer make_buffer(Device* self, const std::shared_ptr<DeviceImpl>& d, ElemType 
     std::lock_guard<std::mutex> l(d->issue_mu);
     int rc = 0;
     st->ptr = d->block_get(cls);
+    if (!st->ptr || zero) d->drain();
     if (!st->ptr) {
       rc = ndx_malloc_async(&st->ptr, cls, d->stream);
       if (rc != 0) {  // out of memory: give the cache back and retry once
@@ -537,14 +626,10 @@ Event Device::enqueue_kernel(const KernelDef& kernel, NdRange range, std::vector
       detail::finish_event(ev.shared_state(), false, impl_->broken_why);
       return ev;
     }
-    ev.mark_exec_start();
-    p.stream = impl_->stream;
-    const int rc = kernel.launch(p);
-    if (rc != 0) {
-      detail::finish_event(ev.shared_state(), false, "kernel " + kernel.name + ": " + ndx_error_string(rc));
-      return ev;
-    }
-    ev.shared_state()->seq.store(++impl_->issued, std::memory_order_release);
+    // stream position now, the launch itself on the launcher thread
+    const std::uint64_t seq = ++impl_->issued;
+    ev.shared_state()->seq.store(seq, std::memory_order_release);
+    impl_->push_launch(DeviceImpl::LaunchJob{p, kernel.launch, ev.shared_state(), seq, kernel.name});
     return ev;
   }
 

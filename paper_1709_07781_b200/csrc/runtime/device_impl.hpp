@@ -15,6 +15,7 @@
 
 #include "ndactor/device.hpp"
 #include "ndactor/event.hpp"
+#include "ndactor/kernel.hpp"
 
 namespace ndactor {
 
@@ -62,6 +63,31 @@ struct DeviceImpl : std::enable_shared_from_this<DeviceImpl> {
   std::mutex defer_mu;
   std::condition_variable defer_cv;
   std::size_t deferred = 0;
+
+  // Launch pipeline.  Kernels on the direct path (every dependency already
+  // on this stream) get their stream position at enqueue time and are handed,
+  // in that order, to one launcher thread: the enqueuing thread (an actor)
+  // goes on with its message while the ~2.5 us cudaLaunchKernel runs on
+  // another core.  Every other stream operation first drains the queue, so
+  // issue order stays stream order.
+  struct LaunchJob {
+    LaunchParams p;
+    Launcher launch;
+    std::shared_ptr<Event::State> ev;
+    std::uint64_t seq = 0;
+    std::string name;
+  };
+  std::mutex q_mu;
+  std::condition_variable q_cv;
+  std::deque<LaunchJob> q;
+  bool q_stop = false;
+  bool q_sleeping = false;
+  std::atomic<std::uint64_t> q_pushed{0}, q_done{0};
+  std::atomic<std::uint64_t> launched{0};  // stream position actually issued
+  std::thread launcher;
+  void launcher_loop();
+  void push_launch(LaunchJob&& j);  // caller holds issue_mu
+  void drain();                     // caller holds issue_mu: every pushed job issued
 
   std::atomic<std::size_t> live{0};
   std::atomic<std::uint64_t> next_buffer_id{1};
