@@ -1,6 +1,6 @@
 #!/bin/bash
-# One GPU session: parity tests, bench, ncu launch list, ncu --set full of the
-# hot kernels.  Outputs under gpurun_out/$TAG.
+# One GPU session: parity tests, bench, reference arm, stage times, ncu launch
+# list, ncu --set full of the hot kernels.  Outputs under gpurun_out/$TAG.
 TAG=${TAG:-r1}
 O=gpurun_out/$TAG
 mkdir -p $O
@@ -16,6 +16,8 @@ cat $O/stages_c3.txt $O/stages_c4.txt | tail -8
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv \
   python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
 for C in C4 C3; do
-ncu --set full --clock-control none --import-source on -k regex:"k_hist|k_plan|k_pass|k_emit|k_table" -c 9 \
-  -o $O/full_$C -f python tools/stage_times.py $C --reps 1 > $O/ncu_full_$C.log 2>&1; echo "ncu full $C rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"k_hist|k_plan|k_pass" -c 9 \
+  -o $O/full_sort_$C -f python tools/stage_times.py $C --reps 1 > $O/ncu_full_sort_$C.log 2>&1; echo "ncu sort $C rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"k_emit|k_table" -c 2 \
+  -o $O/full_emit_$C -f python tools/stage_times.py $C --reps 1 > $O/ncu_full_emit_$C.log 2>&1; echo "ncu emit $C rc=$?"
 done
