@@ -30,7 +30,13 @@
 
 namespace ndx {
 
-constexpr int kEmitThreads = 128;
+#ifndef NDX_EMIT_THREADS
+#define NDX_EMIT_THREADS 256
+#endif
+#ifndef NDX_EMIT_MINB
+#define NDX_EMIT_MINB 3
+#endif
+constexpr int kEmitThreads = NDX_EMIT_THREADS;
 constexpr int kEmitWarps = kEmitThreads / 32;
 constexpr int kEmitK = 8;                               // consecutive elements per thread
 constexpr int kEmitTile = kEmitThreads * kEmitK;        // 1024
@@ -206,31 +212,47 @@ template <bool SMALL>
 __device__ __forceinline__ void span_emit(const Span& s, const uint64_t* Bs, uint32_t carry,
                                           uint32_t o, uint32_t h, uint32_t* stage, uint32_t* hv,
                                           uint32_t* ho) {
+  // shared-space addresses, bumped per word: one STS per word, no generic
+  // address arithmetic
+  uint32_t sa = smem_addr(stage) + 4u * o;
   uint32_t acc = carry;
   if (s.vmask == 0 && s.first_body == 1) {
 #pragma unroll
     for (int j = 0; j < kEmitK; ++j) {
       const uint32_t gap = gap_of<SMALL>(s.pk[j]), bit = bit_of<SMALL>(s.pk[j], Bs[j]);
-      if (gap) stage[o++] = kFillFlag | gap;
+      if (gap) {
+        sts_u32(sa, kFillFlag | gap);
+        sa += 4;
+      }
       acc = ((s.hmask >> j) & 1u) ? bit : (acc | bit);
-      if ((s.tmask >> j) & 1u) stage[o++] = acc;
+      if ((s.tmask >> j) & 1u) {
+        sts_u32(sa, acc);
+        sa += 4;
+      }
     }
     return;
   }
+  const uint32_t sbase = smem_addr(stage);
 #pragma unroll
   for (int j = 0; j < kEmitK; ++j) {
     const uint32_t gap = gap_of<SMALL>(s.pk[j]), bit = bit_of<SMALL>(s.pk[j], Bs[j]);
     if ((s.vmask >> j) & 1u) {
       hv[h] = pkey(Bs[j]);
-      ho[h] = o;
+      ho[h] = (sa - sbase) >> 2;
       ++h;
     }
-    if (gap) stage[o++] = kFillFlag | gap;
+    if (gap) {
+      sts_u32(sa, kFillFlag | gap);
+      sa += 4;
+    }
     acc = ((s.hmask >> j) & 1u) ? bit : (acc | bit);
     if ((s.tmask >> j) & 1u) {
       const bool first = (s.hmask & ((2u << j) - 1u)) == 0;
       const uint32_t body = (first && s.first_body != 1) ? s.first_body : acc;
-      if (body) stage[o++] = body;
+      if (body) {
+        sts_u32(sa, body);
+        sa += 4;
+      }
     }
   }
 }
@@ -274,7 +296,7 @@ __device__ __forceinline__ void tile_phase1(bool full, const uint64_t* B,
     span_scan<SMALL, false>(B, pairs, n, ts, li0, sp);
 }
 
-__global__ __launch_bounds__(kEmitThreads, 6) void k_emit(const uint64_t* __restrict__ pairs,
+__global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint64_t* __restrict__ pairs,
                                                           uint64_t n, Ctl* ctl,
                                                           uint32_t* __restrict__ words,
                                                           uint32_t* __restrict__ vstart,
