@@ -45,7 +45,10 @@ def test_error_strings_and_sizes_without_gpu():
     assert b"invalid" in lib.ndx_error_string(10001)
     assert b"2^31" in lib.ndx_error_string(10002)
     assert lib.ndx_wah_ctl_bytes() % 256 == 0
-    assert lib.ndx_wah_status_bytes(1 << 20) >= 2048 * 8 * 256
+    # one u64 status per (tile, digit) of the pass with the most: the wide
+    # pass has 16384-pair tiles x 2048 digits, the byte passes 8192 x 256
+    n = 1 << 20
+    assert lib.ndx_wah_status_bytes(n) >= 256 + max((n // 16384) * 2048, (n // 8192) * 256) * 8
     assert lib.ndx_wah_emit_scratch_bytes(1 << 20) > 0
     assert lib.ndx_scan_scratch_bytes(5000) > 0
 
