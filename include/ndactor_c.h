@@ -42,6 +42,20 @@ int ndactor_wah_build_index(ndactor_runtime* rt, const uint32_t* values, uint64_
                             uint32_t* entries, uint64_t entries_cap,
                             uint64_t* n_words, uint64_t* n_entries);
 
+/* Pipelined variant of ndactor_wah_build_index for a stream of columns:
+ * returns at once.  The upload of `values` (pinned host memory) runs on its
+ * own stream, so it overlaps the previous build and the previous result's
+ * copy to the host; the result (counts, then up to words_cap words and
+ * entries_cap table words, all pinned host memory) is written by the GPU
+ * with no host round trip for the sizes.  At most two builds in flight:
+ * call ndactor_wah_wait(ticket) before reusing a ticket's buffers.  The
+ * inputs must stay untouched until then.  counts->words / ->distinct give
+ * the true sizes even if the capacities were too small. */
+int ndactor_wah_build_index_async(ndactor_runtime* rt, const uint32_t* values, uint64_t n,
+                                  uint32_t* words, uint64_t words_cap, uint32_t* entries,
+                                  uint64_t entries_cap, ndx_wah_counts* counts, uint64_t* ticket);
+int ndactor_wah_wait(ndactor_runtime* rt, uint64_t ticket);
+
 /* The same chain on keys already resident on the device (d_keys: n u32, not
  * modified; row ids start at row_base).  The result stays on the device:
  * *d_counts points at an ndx_wah_counts {words, distinct, min, max},

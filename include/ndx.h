@@ -113,6 +113,15 @@ int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart,
                   uint64_t n, const void* d_ctl, uint32_t* d_entries,
                   void* stream);
 
+/* Result copy-out with no host round trip for the sizes: a kernel reads W and
+ * D from ctl and writes the counts, min(W, words_cap) words and
+ * min(3D, entries_cap) table words straight into host memory.  h_* must be
+ * pinned (device-accessible) host memory; the data is there once the
+ * stream reaches this point. */
+int ndx_wah_copy_out(const void* d_ctl, const uint32_t* d_words, const uint32_t* d_entries,
+                     ndx_wah_counts* h_counts, uint32_t* h_words, uint64_t words_cap,
+                     uint32_t* h_entries, uint64_t entries_cap, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Multi-GPU build: shards of rows [S_g, S_{g+1}),
  * S_g = 0 mod 31, are built with row_base = S_g; the pieces are then merged.

@@ -546,3 +546,56 @@ int ndx_wah_table(const uint32_t* d_values, const uint32_t* d_vstart, uint64_t n
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Result copy-out without a host round trip for the sizes: one kernel reads
+// W and D from ctl and writes the counts, the words and the table straight
+// into pinned (device-accessible) host memory over PCIe.
+
+namespace ndx {
+
+__global__ void k_copy_out(const Ctl* __restrict__ ctl, const uint32_t* __restrict__ words,
+                           const uint32_t* __restrict__ entries, ndx_wah_counts* h_counts,
+                           uint32_t* h_words, uint64_t words_cap, uint32_t* h_entries,
+                           uint64_t entries_cap) {
+  const uint64_t W = ctl->words, D = ctl->distinct;
+  const uint64_t nw = umin(W, words_cap), ne = umin(3 * D, entries_cap);
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(h_words) & 15) == 0) {
+    const uint64_t n4 = nw / 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(words);
+    uint4* d4 = reinterpret_cast<uint4*>(h_words);
+    for (uint64_t i = tid; i < n4; i += stride) d4[i] = ldg_stream4(s4 + i);
+    for (uint64_t i = 4 * n4 + tid; i < nw; i += stride) h_words[i] = words[i];
+  } else {
+    for (uint64_t i = tid; i < nw; i += stride) h_words[i] = words[i];
+  }
+  for (uint64_t i = tid; i < ne; i += stride) h_entries[i] = entries[i];
+  if (tid == 0) {
+    ndx_wah_counts c;
+    c.words = W;
+    c.distinct = D;
+    c.min_key = ctl->min_key;
+    c.max_key = ctl->max_key;
+    *h_counts = c;
+  }
+}
+
+}  // namespace ndx
+
+extern "C" int ndx_wah_copy_out(const void* d_ctl, const uint32_t* d_words,
+                                const uint32_t* d_entries, ndx_wah_counts* h_counts,
+                                uint32_t* h_words, uint64_t words_cap, uint32_t* h_entries,
+                                uint64_t entries_cap, void* stream) {
+  if (!d_ctl || !d_words || !d_entries || !h_counts || (!h_words && words_cap) ||
+      (!h_entries && entries_cap))
+    return NDX_E_INVALID;
+  int sms = 0;
+  int rc = ndx::sm_count(&sms);
+  if (rc) return rc;
+  ndx::k_copy_out<<<sms * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const ndx::Ctl*>(d_ctl), d_words, d_entries, h_counts, h_words, words_cap,
+      h_entries, entries_cap);
+  return cudaGetLastError();
+}

@@ -22,6 +22,26 @@ struct ndactor_runtime {
   std::uint32_t shard_base = 0;
   wah::DeviceIndex last;   // result of the last device build (kept alive)
   ActorHandle probe;
+  // pipelined host builds: uploads run on their own stream (the other copy
+  // direction of the PCIe link) while the previous build and its result
+  // copy run on the device stream
+  struct Slot {
+    Buffer keys;
+    std::uint64_t cap = 0;
+    void* uploaded = nullptr;  // cudaEvent: keys are on the device
+    void* done = nullptr;      // cudaEvent: the result is in host memory
+    bool busy = false;
+  };
+  void* upload = nullptr;
+  Slot slots[2];
+  std::uint64_t next_ticket = 0;
+  ~ndactor_runtime() {
+    for (Slot& s : slots) {
+      if (s.uploaded) ndx_event_destroy(s.uploaded);
+      if (s.done) ndx_event_destroy(s.done);
+    }
+    if (upload) ndx_stream_destroy(upload);
+  }
 };
 
 namespace {
@@ -118,6 +138,76 @@ int ndactor_wah_build_index(ndactor_runtime* rt, const uint32_t* values, uint64_
     release(d.entries);
     if (n_words) *n_words = c.words;
     if (n_entries) *n_entries = c.distinct;
+    return 0;
+  });
+}
+
+int ndactor_wah_build_index_async(ndactor_runtime* rt, const uint32_t* values, uint64_t n,
+                                  uint32_t* words, uint64_t words_cap, uint32_t* entries,
+                                  uint64_t entries_cap, ndx_wah_counts* counts, uint64_t* ticket) {
+  return guarded([&] {
+    if (!rt || !counts || !ticket) throw std::invalid_argument("null argument");
+    if (n == 0) throw std::invalid_argument("empty input");
+    Device& dev = *rt->dev;
+    auto ck = [](int rc, const char* what) {
+      if (rc) throw std::runtime_error(std::string(what) + ": " + ndx_error_string(rc));
+    };
+    if (!rt->upload) ck(ndx_stream_create(&rt->upload), "upload stream");
+    const std::uint64_t t = rt->next_ticket;
+    ndactor_runtime::Slot& sl = rt->slots[t & 1];
+    if (sl.busy) throw std::runtime_error("two builds already in flight: wait for one first");
+    if (!sl.uploaded) ck(ndx_event_create(&sl.uploaded, 0), "event");
+    if (!sl.done) ck(ndx_event_create(&sl.done, 0), "event");
+    if (sl.cap < n) {
+      if (sl.keys.valid()) {
+        dev.await_all();
+        dev.free_buffer(sl.keys);
+      }
+      sl.keys = dev.create_buffer_uninit(ElemType::u32, std::int64_t(n));
+      sl.cap = n;
+      dev.await_all();
+    }
+    // the slot's keys were last read by build t-2: its `done` orders the upload
+    ck(ndx_stream_wait_event(rt->upload, sl.done), "upload wait");
+    ck(ndx_memcpy_h2d_async(sl.keys.data(), values, n * 4, rt->upload), "upload");
+    ck(ndx_event_record(sl.uploaded, rt->upload), "upload record");
+    void* up = sl.uploaded;
+    Event ready = dev.enqueue_native("wait_upload", [up](void* s) { return ndx_stream_wait_event(s, up); }, {});
+    // the chain releases its input MemRef: hand it a non-owning view of the slot
+    Buffer view = dev.wrap_buffer(sl.keys.data(), ElemType::u32, std::int64_t(n), Access::read_only);
+    wah::DeviceIndex d = wah::build_index_device(*rt->sys, rt->stages, MemRef(view, ready), std::uint32_t(n));
+    void* done = sl.done;
+    std::vector<Event> deps{d.entries.pending(), d.words.pending(), d.cfg.pending()};
+    const void* cfg = d.cfg.buffer().data();
+    const uint32_t* dw = static_cast<const uint32_t*>(d.words.buffer().data());
+    const uint32_t* de = static_cast<const uint32_t*>(d.entries.buffer().data());
+    dev.enqueue_native(
+        "copy_out",
+        [=](void* s) -> int {
+          int rc = ndx_wah_copy_out(cfg, dw, de, counts, words, words_cap, entries, entries_cap, s);
+          if (!rc) rc = ndx_event_record(done, s);
+          return rc;
+        },
+        deps);
+    release(d.cfg);
+    release(d.words);
+    release(d.entries);
+    sl.busy = true;
+    rt->next_ticket = t + 1;
+    *ticket = t;
+    return 0;
+  });
+}
+
+int ndactor_wah_wait(ndactor_runtime* rt, uint64_t ticket) {
+  return guarded([&] {
+    if (!rt) throw std::invalid_argument("null runtime");
+    ndactor_runtime::Slot& sl = rt->slots[ticket & 1];
+    if (!sl.busy) return 0;
+    (void)rt->dev->stream();  // every queued launch issued before waiting on the event
+    const int rc = ndx_event_synchronize(sl.done);
+    sl.busy = false;
+    if (rc) throw std::runtime_error(std::string("build failed: ") + ndx_error_string(rc));
     return 0;
   });
 }

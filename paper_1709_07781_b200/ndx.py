@@ -61,6 +61,7 @@ SIGNATURES = [
     ("ndx_wah_sort", ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp]),
     ("ndx_wah_emit", ctypes.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ndx_wah_table", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    ("ndx_wah_copy_out", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u64, _vp]),
     ("ndx_wah_shard_meta", ctypes.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_wah_assemble", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     ("ndx_scan_scratch_bytes", _sz, [_u64]),

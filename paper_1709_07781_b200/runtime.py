@@ -46,6 +46,9 @@ def load() -> ctypes.CDLL:
             "ndactor_dispatch_probe": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(ctypes.c_double),
                                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
             "ndactor_dispatch_probe_ex": (ctypes.c_int, [_vp, _u64, ctypes.POINTER(ctypes.c_double)]),
+            "ndactor_wah_build_index_async": (ctypes.c_int, [_vp, _vp, _u64, _vp, _u64, _vp, _u64, _vp,
+                                                             ctypes.POINTER(_u64)]),
+            "ndactor_wah_wait": (ctypes.c_int, [_vp, _u64]),
             "ndactor_shard_bounds": (ctypes.c_int, [_u64, ctypes.c_uint32, _vp]),
             "ndactor_merge_plan": (ctypes.c_int, [ctypes.c_uint32, _vp, _vp, _vp, _vp, ctypes.POINTER(_u64),
                                                   ctypes.POINTER(_u64)]),
@@ -100,6 +103,21 @@ class Runtime:
                                                 words.size, ent.ctypes.data, ent.size, ctypes.byref(nw),
                                                 ctypes.byref(ne)), "build_index")
         return n, ent[: 3 * ne.value].reshape(-1, 3), words[: nw.value]
+
+    def build_index_async(self, values: np.ndarray, words_out: np.ndarray, entries_out: np.ndarray,
+                          counts_out: np.ndarray) -> int:
+        """Pipelined build (ndactor_wah_build_index_async): all four arrays
+        must be pinned host memory and stay untouched until wait(ticket).
+        counts_out: 3 x u64 (words, distinct, min | max << 32)."""
+        v = values
+        t = _u64()
+        _check(self.lib.ndactor_wah_build_index_async(
+            self.h, v.ctypes.data, v.size, words_out.ctypes.data, words_out.size, entries_out.ctypes.data,
+            entries_out.size, counts_out.ctypes.data, ctypes.byref(t)), "build_index_async")
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        _check(self.lib.ndactor_wah_wait(self.h, ticket), "wait")
 
     def build_index_device(self, d_keys: int, n: int, row_base: int = 0):
         """Enqueue the chain on device keys; returns device pointers

@@ -55,3 +55,37 @@ def test_runtime_dispatch_probe_counts_every_kernel():
     assert check == 4000
     assert raw_ms > 0 and actor_ms > 0
     rt.close()
+
+
+@pytest.mark.gpu
+def test_runtime_async_pipeline_matches_oracle(port):
+    """ndactor_wah_build_index_async: two builds in flight, results written
+    by the GPU straight into pinned host memory, bit-exact."""
+    import torch
+
+    from paper_1709_07781_b200 import gen
+    from paper_1709_07781_b200.runtime import Runtime
+
+    rt = Runtime()
+    cols = [gen.uniform(11, 300_000, 1000), gen.zipf(5, 500_000, 4096, 1.0), gen.uniform(12, 77_777, 3),
+            np.full(40_000, 9, np.uint32)]
+    pin = lambda k: torch.empty(k, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)  # noqa: E731
+    ins = [pin(v.size) for v in cols]
+    for a, v in zip(ins, cols):
+        a[:] = v
+    outs = [(pin(2 * v.size), pin(3 * 4096 + 64), torch.zeros(3, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64))
+            for v in cols]
+    pending = []
+    for i, v in enumerate(cols):
+        if len(pending) == 2:
+            j, t = pending.pop(0)
+            rt.wait(t)
+        pending.append((i, rt.build_index_async(ins[i], *outs[i])))
+    for _, t in pending:
+        rt.wait(t)
+    for v, (w, e, c) in zip(cols, outs):
+        ref = port.reference_index(v)
+        W, D = int(c[0]), int(c[1])
+        assert W == ref.words.size and D == len(ref.entries)
+        assert np.array_equal(w[:W], ref.words) and np.array_equal(e[:3 * D].reshape(-1, 3), ref.entries)
+    rt.close()
