@@ -50,15 +50,38 @@ inline void cpu_relax() {
 }
 }  // namespace
 
-void DeviceImpl::push_launch(LaunchJob&& j) {
-  bool wake;
-  {
-    std::lock_guard<std::mutex> l(q_mu);
-    q.push_back(std::move(j));
-    wake = q_sleeping;
+void DeviceImpl::push_launch(const LaunchParams& p, const Launcher& launch,
+                             const std::shared_ptr<Event::State>& ev, std::uint64_t seq,
+                             const std::string& name) {
+  const std::uint64_t t = q_pushed.load(std::memory_order_relaxed);
+  for (unsigned i = 0; t - q_done.load(std::memory_order_acquire) >= kRing; ++i)
+    if (i > 64) std::this_thread::yield();  // ring full: the launcher is behind
+  LaunchJob& j = ring[t % kRing];
+  LaunchParams& q = j.p;
+  q.rank = p.rank;
+  q.grid = p.grid;
+  q.block = p.block;
+  q.offset = p.offset;
+  q.global = p.global;
+  q.shared_bytes = p.shared_bytes;
+  q.nargs = p.nargs;
+  for (std::size_t i = 0; i < p.nargs; ++i) {
+    q.ptr[i] = p.ptr[i];
+    q.len[i] = p.len[i];
+    q.smem_offset[i] = p.smem_offset[i];
+    q.scalar[i] = p.scalar[i];
   }
-  q_pushed.fetch_add(1, std::memory_order_release);
-  if (wake) q_cv.notify_one();
+  j.launch = launch;
+  j.ev = ev;
+  j.seq = seq;
+  j.name = name;
+  // seq_cst pair with the launcher's (store sleeping, load pushed): one of
+  // the two sides always sees the other
+  q_pushed.store(t + 1, std::memory_order_seq_cst);
+  if (q_sleeping.load(std::memory_order_seq_cst)) {
+    std::lock_guard<std::mutex> l(q_mu);
+    q_cv.notify_one();
+  }
 }
 
 void DeviceImpl::drain() {
@@ -72,43 +95,34 @@ void DeviceImpl::drain() {
 }
 
 void DeviceImpl::launcher_loop() {
-  std::deque<LaunchJob> batch;
+  std::uint64_t h = 0;
   for (;;) {
-    {
-      std::unique_lock<std::mutex> l(q_mu);
-      if (q.empty()) {
-        // a chain of requests arrives every ~microsecond: spin briefly
-        // before sleeping so a steady stream never pays a wake-up
-        l.unlock();
-        for (int i = 0; i < 20000 && q_pushed.load(std::memory_order_acquire) ==
-                                         q_done.load(std::memory_order_relaxed);
-             ++i)
-          cpu_relax();
-        l.lock();
-        if (q.empty()) {
-          q_sleeping = true;
-          q_cv.wait(l, [&] { return q_stop || !q.empty(); });
-          q_sleeping = false;
-        }
-        if (q.empty()) return;  // stopping
+    std::uint64_t t = q_pushed.load(std::memory_order_acquire);
+    if (h == t) {
+      // a chain of requests arrives every microsecond or so: spin briefly
+      // before sleeping so a steady stream never pays a wake-up
+      for (int i = 0; i < 20000 && (t = q_pushed.load(std::memory_order_acquire)) == h; ++i) cpu_relax();
+      if (h == t) {
+        std::unique_lock<std::mutex> l(q_mu);
+        q_sleeping.store(true, std::memory_order_seq_cst);
+        q_cv.wait(l, [&] { return q_stop || q_pushed.load(std::memory_order_seq_cst) != h; });
+        q_sleeping.store(false, std::memory_order_release);
+        t = q_pushed.load(std::memory_order_acquire);
+        if (h == t) return;  // stopping
       }
-      batch.swap(q);
     }
-    for (LaunchJob& j : batch) {
-      {
-        auto& es = *j.ev;
-        if (!es.exec_started.exchange(true)) {
-          std::lock_guard<std::mutex> l(es.mu);
-          es.exec_start_tp = Clock::now();
-        }
-      }
+    for (; h < t; ++h) {
+      LaunchJob& j = ring[h % kRing];
       j.p.stream = stream;
       const int rc = j.launch(j.p);
       if (rc != 0) finish_event(j.ev, false, "kernel " + j.name + ": " + ndx_error_string(rc));
+      // drop what the job holds now (a launcher may own device resources
+      // that must not outlive the Device)
+      j.ev.reset();
+      j.launch = nullptr;
       launched.store(j.seq, std::memory_order_release);
-      q_done.fetch_add(1, std::memory_order_release);
+      q_done.store(h + 1, std::memory_order_release);
     }
-    batch.clear();
   }
 }
 
@@ -628,8 +642,9 @@ Event Device::enqueue_kernel(const KernelDef& kernel, NdRange range, std::vector
     }
     // stream position now, the launch itself on the launcher thread
     const std::uint64_t seq = ++impl_->issued;
+    ev.mark_exec_start();  // handed to the stream's launcher now
     ev.shared_state()->seq.store(seq, std::memory_order_release);
-    impl_->push_launch(DeviceImpl::LaunchJob{p, kernel.launch, ev.shared_state(), seq, kernel.name});
+    impl_->push_launch(p, kernel.launch, ev.shared_state(), seq, kernel.name);
     return ev;
   }
 

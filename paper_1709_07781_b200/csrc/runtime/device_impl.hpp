@@ -77,16 +77,21 @@ struct DeviceImpl : std::enable_shared_from_this<DeviceImpl> {
     std::uint64_t seq = 0;
     std::string name;
   };
+  // single-producer (under issue_mu) / single-consumer ring: a push copies
+  // only the arguments the kernel has, so little crosses between cores
+  static constexpr std::size_t kRing = 8192;
+  std::unique_ptr<LaunchJob[]> ring{new LaunchJob[kRing]};
   std::mutex q_mu;
   std::condition_variable q_cv;
-  std::deque<LaunchJob> q;
   bool q_stop = false;
-  bool q_sleeping = false;
+  std::atomic<bool> q_sleeping{false};
   std::atomic<std::uint64_t> q_pushed{0}, q_done{0};
   std::atomic<std::uint64_t> launched{0};  // stream position actually issued
   std::thread launcher;
   void launcher_loop();
-  void push_launch(LaunchJob&& j);  // caller holds issue_mu
+  // caller holds issue_mu
+  void push_launch(const LaunchParams& p, const Launcher& launch,
+                   const std::shared_ptr<Event::State>& ev, std::uint64_t seq, const std::string& name);
   void drain();                     // caller holds issue_mu: every pushed job issued
 
   std::atomic<std::size_t> live{0};
