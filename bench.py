@@ -118,6 +118,7 @@ def dist_setup(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ["NCCL_DEBUG"] = "WARN"  # stdout carries exactly one JSON line
         if args.impl == "ours":
             torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo", rank=rank, world_size=world)
@@ -207,13 +208,8 @@ def run_sharded(args, cfg, world, rank, local):
 
     def step(k):
         W, D, meta_d = sb.build(k, n_r, base)
-        meta = meta_d[: D * 8].cpu().numpy().view(shard.META_DTYPE)
-        metas = shard.exchange_meta(meta)
-        entries, pieces, total = shard.plan_merge(metas)
-        if state.get("cap", 0) < total:
-            state["out"] = torch.empty(total, dtype=torch.int32, device=dev)
-            state["cap"] = total
-        shard.assemble([sb.words[:W]], [pieces[rank]], total, dev, out=state["out"])
+        metas, sizes = shard.exchange_meta_device(meta_d, D)
+        entries, pieces, total = shard.plan_merge(metas, sizes)
         state.update(W=W, D=D, entries=entries, pieces=pieces, total=total)
 
     def barrier():
@@ -246,11 +242,12 @@ def run_sharded(args, cfg, world, rank, local):
     value = total_values / (ms * 1e-3)
 
     # the gathered index on rank 0 (words over NVLink, then all pieces placed)
+    out = torch.empty(max(state["total"], 1), dtype=torch.int32, device=dev) if rank == 0 else None
     barrier()
     g0 = time.perf_counter()
     staged = shard.gather_words(sb.words[: state["W"]], dst=0)
     if rank == 0:
-        shard.assemble(staged, state["pieces"], state["total"], dev, out=state["out"])
+        shard.assemble(staged, state["pieces"], state["total"], dev, out=out)
     barrier()
     gather_ms = max_over_ranks((time.perf_counter() - g0) * 1e3)
 
@@ -276,8 +273,9 @@ def run_sharded(args, cfg, world, rank, local):
                    "parallelism": f"row shards x{world} (31-aligned), NCCL metadata all-gather, "
                                   f"boundary merge (SURVEY App. B)",
                    "words": state["total"], "distinct": int(len(state["entries"])),
-                   "path": "per-rank 4-stage build + shard meta + all-gather + merge plan + own pieces "
-                           "into final form; gather to rank 0 timed separately"},
+                   "path": "per-rank 4-stage build (global row ids) + shard metadata kernel + NCCL "
+                           "all-gather of the metadata + merge plan (every rank knows where each of "
+                           "its words goes); the gather of all words to rank 0 is timed separately"},
         "gather_to_rank0_ms": gather_ms,
         "e2e": {"value": total_values / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
                 "d2h_bytes_per_step": 4 * state["W"], "ms_per_step": e2e_ms},

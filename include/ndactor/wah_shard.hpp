@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <span>
+#include <utility>
 #include <vector>
 
 #include "ndactor/wah.hpp"
@@ -32,5 +33,12 @@ struct MergePlan {
 /// previous piece, or -- at gap 0 when both sides are ones-fills -- one fused
 /// ones-fill that replaces the previous last word and its own first word.
 MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards);
+
+/// The same, writing straight into caller storage: entries_out (capacity:
+/// the total record count) and pieces_out[g][i] for record i of shard g.
+/// Returns the merged (entries, words) counts.
+std::pair<std::uint64_t, std::uint64_t> plan_merge_into(
+    std::span<const std::span<const ndx_shard_meta>> shards, IndexEntry* entries_out,
+    std::span<ndx_piece* const> pieces_out);
 
 }  // namespace ndactor::wah

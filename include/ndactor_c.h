@@ -94,13 +94,14 @@ void ndactor_gen_instances(uint32_t seed, uint32_t count, const uint32_t* cards,
  * bounds[0..shards]: row shard bounds, inner ones multiples of 31. */
 int ndactor_shard_bounds(uint64_t n, uint32_t shards, uint64_t* bounds);
 /* Merge plan over the shards' metadata (ndx_wah_shard_meta of each shard,
- * concatenated in shard order, counts[g] records each).  Writes the merged
- * (value, offset, length) entries (capacity: sum of counts) and one
- * ndx_piece per input record (same order); the pieces' src_off are local to
- * their shard's words. */
+ * counts[g] records each; shard g starts at metas + g*stride, or the shards
+ * are concatenated when stride is 0).  Writes the merged (value, offset,
+ * length) entries (capacity: sum of counts) and one ndx_piece per input
+ * record at the same position (dst absolute in the merged words; src_off
+ * local to the shard's words). */
 int ndactor_merge_plan(uint32_t shards, const ndx_shard_meta* metas, const uint64_t* counts,
-                       uint32_t* entries, ndx_piece* pieces, uint64_t* n_entries,
-                       uint64_t* n_words);
+                       uint64_t stride, uint32_t* entries, ndx_piece* pieces,
+                       uint64_t* n_entries, uint64_t* n_words);
 
 /* "WAH1" index file (p/core/src/wah_index_io.cpp:30-87). */
 int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_t* entries,

@@ -362,28 +362,22 @@ int ndactor_shard_bounds(uint64_t n, uint32_t shards, uint64_t* bounds) {
 }
 
 int ndactor_merge_plan(uint32_t shards, const ndx_shard_meta* metas, const uint64_t* counts,
-                       uint32_t* entries, ndx_piece* pieces, uint64_t* n_entries,
+                       uint64_t stride, uint32_t* entries, ndx_piece* pieces, uint64_t* n_entries,
                        uint64_t* n_words) {
   return guarded([&] {
+    static_assert(sizeof(wah::IndexEntry) == 12, "IndexEntry must be three u32");
     std::vector<std::span<const ndx_shard_meta>> sh(shards);
+    std::vector<ndx_piece*> outs(shards);
     std::uint64_t off = 0;
     for (uint32_t g = 0; g < shards; ++g) {
-      sh[g] = std::span<const ndx_shard_meta>(metas + off, counts[g]);
+      const std::uint64_t at = stride ? g * stride : off;
+      sh[g] = std::span<const ndx_shard_meta>(metas + at, counts[g]);
+      outs[g] = pieces + at;
       off += counts[g];
     }
-    const wah::MergePlan plan = wah::plan_merge(sh);
-    for (std::size_t i = 0; i < plan.entries.size(); ++i) {
-      entries[3 * i] = plan.entries[i].value;
-      entries[3 * i + 1] = plan.entries[i].offset;
-      entries[3 * i + 2] = plan.entries[i].length;
-    }
-    off = 0;
-    for (uint32_t g = 0; g < shards; ++g) {
-      std::memcpy(pieces + off, plan.pieces[g].data(), plan.pieces[g].size() * sizeof(ndx_piece));
-      off += counts[g];
-    }
-    *n_entries = plan.entries.size();
-    *n_words = plan.words;
+    auto [ne, nw] = wah::plan_merge_into(sh, reinterpret_cast<wah::IndexEntry*>(entries), outs);
+    *n_entries = ne;
+    *n_words = nw;
     return 0;
   });
 }

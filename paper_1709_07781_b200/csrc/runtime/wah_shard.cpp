@@ -30,23 +30,17 @@ struct LastWord {
 
 }  // namespace
 
-MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
+std::pair<std::uint64_t, std::uint64_t> plan_merge_into(
+    std::span<const std::span<const ndx_shard_meta>> shards, IndexEntry* entries_out,
+    std::span<ndx_piece* const> pieces_out) {
   const std::size_t G = shards.size();
-  MergePlan plan;
-  plan.pieces.resize(G);
-  std::size_t total = 0;
-  for (std::size_t g = 0; g < G; ++g) {
-    plan.pieces[g].resize(shards[g].size());
-    total += shards[g].size();
+  if (pieces_out.size() != G) throw WahError("plan_merge: one piece array per shard");
+  for (std::size_t g = 0; g < G; ++g)
     for (std::size_t i = 1; i < shards[g].size(); ++i)
       if (shards[g][i].value <= shards[g][i - 1].value)
         throw WahError("plan_merge: shard " + std::to_string(g) + " values not ascending");
-  }
-  plan.entries.reserve(total);
   std::vector<std::size_t> head(G, 0);
-  std::vector<std::pair<std::size_t, std::size_t>> group;
-  std::vector<std::pair<ndx_piece*, std::uint64_t>> placed;
-  std::uint64_t out = 0;
+  std::uint64_t out = 0, ne = 0;
   for (;;) {
     // next value: the smallest head over the shards (G is small)
     bool any = false;
@@ -57,20 +51,18 @@ MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
         any = true;
       }
     if (!any) break;
-    group.clear();
-    for (std::size_t g = 0; g < G; ++g)
-      if (head[g] < shards[g].size() && shards[g][head[g]].value == v) group.emplace_back(g, head[g]++);
-
     std::uint64_t len = 0;
     LastWord last;
     std::uint32_t prev_l = 0;
-    placed.clear();
-    for (std::size_t k = 0; k < group.size(); ++k) {
-      const ndx_shard_meta& m = shards[group[k].first][group[k].second];
-      ndx_piece& p = plan.pieces[group[k].first][group[k].second];
-      p = ndx_piece{0, m.body_off, m.body_len, 0, 0};
+    bool first = true;
+    for (std::size_t g = 0; g < G; ++g) {
+      if (head[g] >= shards[g].size() || shards[g][head[g]].value != v) continue;
+      const ndx_shard_meta& m = shards[g][head[g]];
+      ndx_piece& p = pieces_out[g][head[g]];
+      ++head[g];
       if (m.body_len == 0) throw WahError("plan_merge: empty body");
-      if (k == 0) {
+      p = ndx_piece{0, m.body_off, m.body_len, 0, 0};
+      if (first) {
         if (m.f > 0) p.lead = make_fill(false, m.f);
       } else {
         if (m.f <= prev_l) throw WahError("plan_merge: shards overlap in chunks");
@@ -89,7 +81,8 @@ MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
           p.src_len -= 1;
         }
       }
-      placed.emplace_back(&p, len);
+      first = false;
+      p.dst = out + len;  // absolute: the value's offset is `out`
       len += (p.lead ? 1u : 0u) + p.src_len;
       if (p.src_len > 0)
         last = LastWord{&p, false, m.z};
@@ -97,12 +90,27 @@ MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
         last = LastWord{&p, true, is_ones_fill(p.lead) ? fill_len(p.lead) : 0u};
       prev_l = m.l;
     }
-    for (auto& [p, r] : placed) p->dst = out + r;
     if (out + len > 0xffffffffull) throw WahError("plan_merge: index exceeds u32 word offsets");
-    plan.entries.push_back(IndexEntry{v, std::uint32_t(out), std::uint32_t(len)});
+    entries_out[ne++] = IndexEntry{v, std::uint32_t(out), std::uint32_t(len)};
     out += len;
   }
-  plan.words = out;
+  return {ne, out};
+}
+
+MergePlan plan_merge(std::span<const std::span<const ndx_shard_meta>> shards) {
+  MergePlan plan;
+  std::size_t total = 0;
+  plan.pieces.resize(shards.size());
+  std::vector<ndx_piece*> outs(shards.size());
+  for (std::size_t g = 0; g < shards.size(); ++g) {
+    plan.pieces[g].resize(shards[g].size());
+    outs[g] = plan.pieces[g].data();
+    total += shards[g].size();
+  }
+  plan.entries.resize(total);
+  auto [ne, nw] = plan_merge_into(shards, plan.entries.data(), outs);
+  plan.entries.resize(ne);
+  plan.words = nw;
   return plan;
 }
 

@@ -50,7 +50,7 @@ def load() -> ctypes.CDLL:
                                                              ctypes.POINTER(_u64)]),
             "ndactor_wah_wait": (ctypes.c_int, [_vp, _u64]),
             "ndactor_shard_bounds": (ctypes.c_int, [_u64, ctypes.c_uint32, _vp]),
-            "ndactor_merge_plan": (ctypes.c_int, [ctypes.c_uint32, _vp, _vp, _vp, _vp, ctypes.POINTER(_u64),
+            "ndactor_merge_plan": (ctypes.c_int, [ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp, ctypes.POINTER(_u64),
                                                   ctypes.POINTER(_u64)]),
             "ndactor_write_index_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, _vp, _u64, _vp, _u64]),
         }

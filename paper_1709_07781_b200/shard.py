@@ -40,24 +40,51 @@ def shard_bounds(n: int, shards: int) -> np.ndarray:
     return out
 
 
-def plan_merge(metas: list[np.ndarray]):
-    """Merge plan over per-shard metadata (each META_DTYPE, ascending values).
+_SCRATCH: dict = {}
 
-    Returns (entries (D,3) u32, pieces list per shard (PIECE_DTYPE), words)."""
+
+def _scratch(name: str, n: int, dtype) -> np.ndarray:
+    """Reused host buffers (fresh pages cost a fault each on first touch).
+    Results returned by plan_merge are views that stay valid until the next
+    call of the same process."""
+    a = _SCRATCH.get(name)
+    if a is None or a.size < n or a.dtype != np.dtype(dtype):
+        a = np.empty(max(n, 1), dtype)
+        a.view(np.uint8)[:] = 0  # touch the pages once
+        _SCRATCH[name] = a
+    return a[:n]
+
+
+def plan_merge(metas, sizes=None):
+    """Merge plan over per-shard metadata (META_DTYPE, ascending values).
+
+    `metas` is a list of per-shard arrays, or a padded (G, cap) array with
+    `sizes` giving each shard's record count (no copy).  Returns (entries
+    (D,3) u32, pieces list per shard (PIECE_DTYPE, dst absolute), words);
+    the arrays are views of reused buffers (copy them to keep them across
+    calls)."""
     lib = _rt.load()
-    counts = np.array([m.size for m in metas], np.uint64)
-    cat = np.ascontiguousarray(np.concatenate(metas) if metas else np.zeros(0, META_DTYPE), META_DTYPE)
+    if sizes is None:
+        counts = np.array([m.size for m in metas], np.uint64)
+        cat = np.ascontiguousarray(np.concatenate(metas) if len(metas) else np.zeros(0, META_DTYPE), META_DTYPE)
+        stride = 0
+        G = len(metas)
+    else:
+        cat = np.ascontiguousarray(metas)
+        G, stride = cat.shape
+        counts = np.asarray(sizes, np.uint64)
     total = int(counts.sum())
-    entries = np.zeros((max(total, 1), 3), np.uint32)
-    pieces = np.zeros(max(total, 1), PIECE_DTYPE)
+    entries = _scratch("entries", max(total, 1) * 3, np.uint32).reshape(-1, 3)
+    pieces = _scratch("pieces", max(cat.size, 1), PIECE_DTYPE)
     ne, nw = ctypes.c_uint64(), ctypes.c_uint64()
-    _rt._check(lib.ndactor_merge_plan(len(metas), cat.ctypes.data, counts.ctypes.data, entries.ctypes.data,
+    _rt._check(lib.ndactor_merge_plan(G, cat.ctypes.data, counts.ctypes.data, stride, entries.ctypes.data,
                                       pieces.ctypes.data, ctypes.byref(ne), ctypes.byref(nw)), "merge_plan")
     out, off = [], 0
-    for c in counts.tolist():
-        out.append(pieces[off:off + c].copy())
+    for g, c in enumerate(counts.tolist()):
+        at = g * stride if stride else off
+        out.append(pieces[at:at + c])
         off += c
-    return entries[: ne.value].copy(), out, int(nw.value)
+    return entries[: ne.value], out, int(nw.value)
 
 
 # ---------------------------------------------------------------------------
@@ -85,6 +112,31 @@ def exchange_meta(meta: np.ndarray, group=None) -> list[np.ndarray]:
     outs = [torch.zeros_like(t) for _ in range(ws)]
     dist.all_gather(outs, t, group=group)
     return [o.cpu().numpy().view(META_DTYPE)[:s].copy() for o, s in zip(outs, sizes)]
+
+
+def exchange_meta_device(meta_d, D: int, group=None):
+    """All-gather of device-resident metadata (meta_d: int32 tensor of at
+    least D*8 words on this rank's GPU) over NCCL, one copy to the host.
+    Returns (padded (G, cap) META_DTYPE array, per-rank record counts) --
+    the form plan_merge takes without copying."""
+    import torch
+    import torch.distributed as dist
+    ws = dist.get_world_size(group)
+    dev = meta_d.device
+    cnt = torch.tensor([D], dtype=torch.int64, device=dev)
+    cnts = torch.empty(ws, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(cnts, cnt, group=group)
+    sizes = cnts.cpu().tolist()
+    cap = max(max(sizes), 1)
+    if meta_d.numel() >= cap * 8:
+        mine = meta_d[: cap * 8]
+    else:
+        mine = torch.zeros(cap * 8, dtype=torch.int32, device=dev)
+        mine[: D * 8] = meta_d[: D * 8]
+    out = torch.empty(ws * cap * 8, dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
+    host = out.cpu().numpy().view(META_DTYPE).reshape(ws, cap)
+    return host, sizes
 
 
 def gather_words(words, dst: int = 0, group=None):
@@ -207,9 +259,8 @@ def build_distributed(values_local: np.ndarray, row_base: int, builder: ShardBui
     keys = torch.from_numpy(np.ascontiguousarray(values_local, np.uint32).view(np.int32)).to(dev)
     n = keys.numel()
     W, D, meta_d = builder.build(keys, n, row_base)
-    meta = meta_d[: D * 8].cpu().numpy().view(META_DTYPE)
-    metas = exchange_meta(meta, group)
-    entries, pieces, total = plan_merge(metas)
+    metas, sizes = exchange_meta_device(meta_d, D, group)
+    entries, pieces, total = plan_merge(metas, sizes)
     staged = gather_words(builder.words[:W], dst=0, group=group)
     if dist.get_rank(group) != 0:
         return entries, None

@@ -121,3 +121,22 @@ def test_split_pieces_same_result(port, block):
     entries, pieces, total = shard.plan_merge(metas)
     split = [shard.split_pieces(p, block) for p in pieces]
     assert np.array_equal(H.assemble(words, split, total), H.assemble(words, pieces, total))
+
+
+def test_merge_plan_padded_input_equals_concatenated(port):
+    v = H.columns()["hot_cold"]
+    b = shard.shard_bounds(v.size, 4).astype(np.int64)
+    metas = []
+    for k in range(4):
+        part = v[b[k]:b[k + 1]]
+        e, w = H.local_index(port, part, int(b[k]))
+        metas.append(H.local_meta(part, int(b[k]), e, w))
+    cap = max(m.size for m in metas) + 3
+    pad = np.zeros((4, cap), shard.META_DTYPE)
+    for g, m in enumerate(metas):
+        pad[g, :m.size] = m
+    e1, p1, w1 = shard.plan_merge(metas)
+    e1, p1 = e1.copy(), [p.copy() for p in p1]  # results are views of reused buffers
+    e2, p2, w2 = shard.plan_merge(pad, [m.size for m in metas])
+    assert w1 == w2 and np.array_equal(e1, e2)
+    assert all(np.array_equal(a, b_) for a, b_ in zip(p1, p2))

@@ -24,16 +24,15 @@ for it in range(4):
     t = [time.perf_counter()]
     W, D, meta_d = sb.build(keys, n, 0)
     torch.cuda.synchronize(); t.append(time.perf_counter())
-    meta = meta_d[: D * 8].cpu().numpy().view(shard.META_DTYPE)
     t.append(time.perf_counter())
-    metas = shard.exchange_meta(meta)
+    metas, sizes = shard.exchange_meta_device(meta_d, D)
     t.append(time.perf_counter())
-    entries, pieces, total = shard.plan_merge(metas)
+    entries, pieces, total = shard.plan_merge(metas, sizes)
     t.append(time.perf_counter())
     if out is None:
         out = torch.empty(total, dtype=torch.int32, device="cuda")
     shard.assemble([sb.words[:W]], [pieces[0]], total, torch.device("cuda"), out=out)
     torch.cuda.synchronize(); t.append(time.perf_counter())
-    print("build %.2f meta_d2h %.2f exchange %.2f plan %.2f assemble %.2f ms" %
+    print("build %.2f - %.2f exchange %.2f plan %.2f assemble %.2f ms" %
           tuple((b - a) * 1e3 for a, b in zip(t, t[1:])))
 dist.destroy_process_group()
