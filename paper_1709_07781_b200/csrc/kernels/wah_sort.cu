@@ -77,19 +77,26 @@ struct Shape {
 
 constexpr int kHistThreads = 512;
 
+// Key range, low-11-bit histogram and byte-1 histogram in one read of the
+// keys.  The byte-0 histogram is the low-11 one folded (2 shared atomics per
+// key, not 3), and every group of four warps counts into its own copy so a
+// skewed column's hot bins are not one shared-memory hot spot.
+constexpr int kHistCopies = 4;
 __global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restrict__ keys,
                                                        uint64_t n, Ctl* ctl) {
-  __shared__ uint32_t h0[256], h1[256], hw[kWideBuckets];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) h0[i] = h1[i] = 0;
-  for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x) hw[i] = 0;
+  __shared__ uint32_t hws[kHistCopies][kWideBuckets], h1s[kHistCopies][256];
+  for (int i = threadIdx.x; i < kHistCopies * kWideBuckets; i += blockDim.x) (&hws[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kHistCopies * 256; i += blockDim.x) (&h1s[0][0])[i] = 0;
   __syncthreads();
+  const int copy = (threadIdx.x >> 5) & (kHistCopies - 1);
+  uint32_t* hw = hws[copy];
+  uint32_t* h1 = h1s[copy];
   uint32_t mx = 0, mxn = 0;
   auto one = [&](uint32_t k) {
     mx = max(mx, k);
     mxn = max(mxn, ~k);
-    atomicAdd(&h0[k & 255u], 1u);
-    atomicAdd(&h1[(k >> 8) & 255u], 1u);
     atomicAdd(&hw[k & (kWideBuckets - 1)], 1u);
+    atomicAdd(&h1[(k >> 8) & 255u], 1u);
   };
   const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -123,12 +130,26 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restric
     atomicMax(&ctl->max_not, mxn);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    if (h0[i]) atomicAdd(&ctl->hist_byte[0][i], h0[i]);
-    if (h1[i]) atomicAdd(&ctl->hist_byte[1][i], h1[i]);
+  for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kHistCopies; ++k) c += hws[k][i];
+    hws[0][i] = c;
+    if (c) atomicAdd(&ctl->hist_wide[i], c);
   }
-  for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x)
-    if (hw[i]) atomicAdd(&ctl->hist_wide[i], hw[i]);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kHistCopies; ++k) c += h1s[k][i];
+    if (c) atomicAdd(&ctl->hist_byte[1][i], c);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < kWideBuckets / 256; ++j) c += hws[0][i + 256 * j];
+    if (c) atomicAdd(&ctl->hist_byte[0][i], c);
+  }
 }
 
 // Histograms of bytes 2 and 3, only when the plan found them varying.

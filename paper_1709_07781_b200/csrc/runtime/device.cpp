@@ -57,24 +57,25 @@ void DeviceImpl::push_launch(const LaunchParams& p, const Launcher& launch,
   for (unsigned i = 0; t - q_done.load(std::memory_order_acquire) >= kRing; ++i)
     if (i > 64) std::this_thread::yield();  // ring full: the launcher is behind
   LaunchJob& j = ring[t % kRing];
-  LaunchParams& q = j.p;
-  q.rank = p.rank;
-  q.grid = p.grid;
-  q.block = p.block;
-  q.offset = p.offset;
-  q.global = p.global;
-  q.shared_bytes = p.shared_bytes;
-  q.nargs = p.nargs;
-  for (std::size_t i = 0; i < p.nargs; ++i) {
-    q.ptr[i] = p.ptr[i];
-    q.len[i] = p.len[i];
-    q.smem_offset[i] = p.smem_offset[i];
-    q.scalar[i] = p.scalar[i];
-  }
-  j.launch = launch;
-  j.ev = ev;
   j.seq = seq;
-  j.name = name;
+  j.ev = ev;
+  j.launch = launch;
+  j.grid = p.grid;
+  j.block = p.block;
+  j.rank = p.rank;
+  j.nargs = unsigned(p.nargs);
+  j.shared_bytes = p.shared_bytes;
+  j.offset = p.offset;
+  j.global = p.global;
+  if (p.nargs > kInlineArgs) j.more.reset(new LaunchArg[p.nargs - kInlineArgs]);
+  for (std::size_t i = 0; i < p.nargs; ++i) {
+    LaunchArg& a = i < kInlineArgs ? j.args[i] : j.more[i - kInlineArgs];
+    a.ptr = p.ptr[i];
+    a.len = p.len[i];
+    a.smem_offset = p.smem_offset[i];
+    a.scalar = p.scalar[i];
+  }
+  j.name_copy = name;
   // seq_cst pair with the launcher's (store sleeping, load pushed): one of
   // the two sides always sees the other
   q_pushed.store(t + 1, std::memory_order_seq_cst);
@@ -96,6 +97,7 @@ void DeviceImpl::drain() {
 
 void DeviceImpl::launcher_loop() {
   std::uint64_t h = 0;
+  LaunchParams lp;  // this thread's own copy, hot in its cache
   for (;;) {
     std::uint64_t t = q_pushed.load(std::memory_order_acquire);
     if (h == t) {
@@ -113,13 +115,28 @@ void DeviceImpl::launcher_loop() {
     }
     for (; h < t; ++h) {
       LaunchJob& j = ring[h % kRing];
-      j.p.stream = stream;
-      const int rc = j.launch(j.p);
-      if (rc != 0) finish_event(j.ev, false, "kernel " + j.name + ": " + ndx_error_string(rc));
+      lp.stream = stream;
+      lp.grid = j.grid;
+      lp.block = j.block;
+      lp.rank = j.rank;
+      lp.nargs = j.nargs;
+      lp.shared_bytes = j.shared_bytes;
+      lp.offset = j.offset;
+      lp.global = j.global;
+      for (unsigned i = 0; i < j.nargs; ++i) {
+        const LaunchArg& a = i < kInlineArgs ? j.args[i] : j.more[i - kInlineArgs];
+        lp.ptr[i] = a.ptr;
+        lp.len[i] = a.len;
+        lp.smem_offset[i] = a.smem_offset;
+        lp.scalar[i] = a.scalar;
+      }
+      const int rc = j.launch(lp);
+      if (rc != 0) finish_event(j.ev, false, "kernel " + j.name_copy + ": " + ndx_error_string(rc));
       // drop what the job holds now (a launcher may own device resources
       // that must not outlive the Device)
       j.ev.reset();
       j.launch = nullptr;
+      j.more.reset();
       launched.store(j.seq, std::memory_order_release);
       q_done.store(h + 1, std::memory_order_release);
     }

@@ -1,6 +1,7 @@
 // Internal: the CUDA device behind ndactor::Device and the Event state.
 #pragma once
 
+#include <array>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
@@ -70,12 +71,28 @@ struct DeviceImpl : std::enable_shared_from_this<DeviceImpl> {
   // goes on with its message while the ~2.5 us cudaLaunchKernel runs on
   // another core.  Every other stream operation first drains the queue, so
   // issue order stays stream order.
-  struct LaunchJob {
-    LaunchParams p;
-    Launcher launch;
-    std::shared_ptr<Event::State> ev;
+  // A queued launch, packed so that the few cache lines it spans are all the
+  // launcher core has to pull from the enqueuing core (the LaunchParams the
+  // kernel's launcher sees is rebuilt in the launcher thread's own copy).
+  struct LaunchArg {
+    void* ptr;
+    std::size_t len;
+    std::size_t smem_offset;
+    Scalar scalar;
+  };
+  static constexpr std::size_t kInlineArgs = 2;
+  struct alignas(64) LaunchJob {
     std::uint64_t seq = 0;
-    std::string name;
+    std::shared_ptr<Event::State> ev;
+    Launcher launch;
+    std::array<unsigned, 3> grid{}, block{};
+    unsigned rank = 1;
+    unsigned nargs = 0;
+    std::size_t shared_bytes = 0;
+    std::array<std::size_t, 3> offset{}, global{};
+    LaunchArg args[kInlineArgs];
+    std::unique_ptr<LaunchArg[]> more;  // arguments past kInlineArgs
+    std::string name_copy;
   };
   // single-producer (under issue_mu) / single-consumer ring: a push copies
   // only the arguments the kernel has, so little crosses between cores
