@@ -56,6 +56,9 @@ namespace ndx {
 #ifndef NDX_SORT_MINB_W
 #define NDX_SORT_MINB_W 1
 #endif
+#ifndef NDX_SORT_LATE_COUNT
+#define NDX_SORT_LATE_COUNT 1
+#endif
 #ifndef NDX_SORT_ATOMRANK
 #define NDX_SORT_ATOMRANK 0
 #endif
@@ -473,14 +476,16 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   }
   __syncthreads();
 
+  uint64_t* st = t.status + tile * NB;
+#if !NDX_SORT_LATE_COUNT
   // ---- early counts: tile histogram, published before the heavy ranking
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r)
     if (FULL || wofs + r * 32 < tile_n) atomicAdd(&t.cnt[((key[r] - t.base) >> t.shift) & DMASK], 1u);
   __syncthreads();
-  uint64_t* st = t.status + tile * NB;
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS)
     st_relaxed_u64(&st[d], st_word(t.epoch, tile == 0 ? kStPrefix : kStAgg, t.cnt[d]));
+#endif
 
   // ---- rank
   uint32_t rank[SH::IPT];
@@ -527,7 +532,15 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       t.H[w * NBMAX + d] = uint16_t(sum);
       sum += c;
     }
+#if NDX_SORT_LATE_COUNT
+    // the tile's digit counts fall out of the warp counters: published here
+    t.cnt[d] = sum;
+    st_relaxed_u64(&st[d], st_word(t.epoch, tile == 0 ? kStPrefix : kStAgg, sum));
+#endif
   }
+#if NDX_SORT_LATE_COUNT
+  __syncthreads();  // the scan reads other threads' counts
+#endif
   block_excl_scan(t.cnt, t.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
 
   // ---- look-back: global base of each digit for this tile
