@@ -59,6 +59,14 @@ namespace ndx {
 #ifndef NDX_SORT_LATE_COUNT
 #define NDX_SORT_LATE_COUNT 1
 #endif
+// narrow-key register packing: measured to help the wide pass (C3 558 ->
+// 546 us) and to hurt the byte passes (C4 3.05 -> 3.14 ms)
+#ifndef NDX_SORT_NARROW_W
+#define NDX_SORT_NARROW_W 1
+#endif
+#ifndef NDX_SORT_NARROW_B
+#define NDX_SORT_NARROW_B 0
+#endif
 #ifndef NDX_SORT_ATOMRANK
 #define NDX_SORT_ATOMRANK 0
 #endif
@@ -400,6 +408,7 @@ struct TileCtx {
   uint64_t* S;               // [tile] staging
   uint32_t* cnt;             // [NB] tile count per digit
   uint32_t* gbase;           // [NB] tile-local start, then global base - local start
+  bool narrow;               // every key < 2^16
 };
 
 // Exclusive count of digit d over all tiles before `tile` (decoupled
@@ -438,10 +447,16 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* st, uint64_t tile, 
 // time, so the ballot match unrolls straight); FULL tiles skip every bounds
 // check.  Element order within a warp is round-major / lane-minor, which is
 // row order, so ranks taken round by round are stable.
-template <class SH, int BITS, int NBMAX, bool FULL>
+// NARROW: every key is below 2^16 (known from the plan), so a pair's rank
+// rides in the upper half of its key register -- 32 fewer live registers in
+// the ranking, no spills.
+template <class SH, int BITS, int NBMAX, bool FULL, bool NARROW>
 __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint32_t tile_n) {
   constexpr uint32_t NB = 1u << BITS;
   constexpr uint32_t DMASK = NB - 1;
+  auto digit = [&](uint32_t k) -> uint32_t {
+    return (((NARROW ? (k & 0xffffu) : k) - t.base) >> t.shift) & DMASK;
+  };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t tile_start = tile * SH::TILE;
   uint16_t* Hw = t.H + warp * NBMAX;
@@ -481,17 +496,17 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   // ---- early counts: tile histogram, published before the heavy ranking
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r)
-    if (FULL || wofs + r * 32 < tile_n) atomicAdd(&t.cnt[((key[r] - t.base) >> t.shift) & DMASK], 1u);
+    if (FULL || wofs + r * 32 < tile_n) atomicAdd(&t.cnt[digit(key[r])], 1u);
   __syncthreads();
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS)
     st_relaxed_u64(&st[d], st_word(t.epoch, tile == 0 ? kStPrefix : kStAgg, t.cnt[d]));
 #endif
 
   // ---- rank
-  uint32_t rank[SH::IPT];
+  uint32_t rank[NARROW ? 1 : SH::IPT];
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r) {
-    const uint32_t d = ((key[r] - t.base) >> t.shift) & DMASK;
+    const uint32_t d = digit(key[r]);
     unsigned peers = warp_match<BITS>(d);
     bool valid = true;
     if (!FULL) {
@@ -511,15 +526,19 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
             0xffffu;
     }
     old = __shfl_sync(kFull, old, leader);
-    rank[r] = old + __popc(peers & lanemask_lt());
+    const uint32_t rk = old + __popc(peers & lanemask_lt());
 #else
     uint32_t old = 0;
     if (lane == leader) old = Hw[d];
     old = __shfl_sync(kFull, old, leader);
     if (valid && lane == leader) Hw[d] = uint16_t(old + __popc(peers));
-    rank[r] = old + __popc(peers & lanemask_lt());
+    const uint32_t rk = old + __popc(peers & lanemask_lt());
     __syncwarp();
 #endif
+    if (NARROW)
+      key[r] |= rk << 16;
+    else
+      rank[r] = rk;
   }
   __syncthreads();
 
@@ -560,13 +579,21 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r) {
-    const uint32_t d = ((key[r] - t.base) >> t.shift) & DMASK;
-    rank[r] += Hw[d];
+    const uint32_t d = digit(key[r]);
+    if (NARROW)
+      key[r] += uint32_t(Hw[d]) << 16;
+    else
+      rank[r] += Hw[d];
   }
   __syncthreads();  // H no longer read: S may overwrite it
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r)
-    if (FULL || wofs + r * 32 < tile_n) t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+    if (FULL || wofs + r * 32 < tile_n) {
+      if (NARROW)
+        t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay[r]) << 32);
+      else
+        t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+    }
   __syncthreads();
 
   // ---- scatter: consecutive local slots of one digit are consecutive globally
@@ -599,10 +626,18 @@ __device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint3
     const uint64_t tile = *s_tile;
     if (tile >= tiles) return;
     const uint32_t tn = uint32_t(umin<uint64_t>(SH::TILE, n - tile * SH::TILE));
-    if (tn == uint32_t(SH::TILE))
-      tile_pass<SH, BITS, NBMAX, true>(t, tile, tn);
-    else
-      tile_pass<SH, BITS, NBMAX, false>(t, tile, tn);
+    constexpr bool kNarrowOk = SH::kWide ? NDX_SORT_NARROW_W : NDX_SORT_NARROW_B;
+    if (tn == uint32_t(SH::TILE)) {
+      if (kNarrowOk && t.narrow)
+        tile_pass<SH, BITS, NBMAX, true, true>(t, tile, tn);
+      else
+        tile_pass<SH, BITS, NBMAX, true, false>(t, tile, tn);
+    } else {
+      if (kNarrowOk && t.narrow)
+        tile_pass<SH, BITS, NBMAX, false, true>(t, tile, tn);
+      else
+        tile_pass<SH, BITS, NBMAX, false, false>(t, tile, tn);
+    }
   }
 }
 
@@ -630,6 +665,7 @@ __global__ __launch_bounds__(Shape<MAXB>::THREADS, Shape<MAXB>::MINB) void k_pas
   t.epoch = pi.epoch;
   t.bstart = pi.bstart;
   t.status = a.status;
+  t.narrow = (MAXB > 8 ? NDX_SORT_NARROW_W : NDX_SORT_NARROW_B) && a.ctl->max_key < 65536u;
   t.H = reinterpret_cast<uint16_t*>(smem);
   t.S = reinterpret_cast<uint64_t*>(smem);
   t.cnt = reinterpret_cast<uint32_t*>(smem + SM::kUnion);
