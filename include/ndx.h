@@ -123,6 +123,38 @@ int ndx_wah_copy_out(const void* d_ctl, const uint32_t* d_words, const uint32_t*
                      uint32_t* h_entries, uint64_t entries_cap, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Query side: decode, bitwise ops, rows, encode.
+ * A decoded bitmap is a chunk array: one u32 per 31-row chunk holding the
+ * chunk's literal (bit i = row 31c + i).
+ * ------------------------------------------------------------------------- */
+/* decode (wah_words.cpp:21-34): chunks[c] for c < n_chunks, zero past the
+ * end of the stream.  d_info[0] = chunks the words cover, d_info[1] = 1 if
+ * a fill has length zero. */
+size_t ndx_wah_decode_scratch_bytes(uint64_t n_words);
+int ndx_wah_decode(const uint32_t* d_words, uint64_t n_words, uint32_t* d_chunks,
+                   uint64_t n_chunks, void* d_scratch, uint32_t* d_info, void* stream);
+/* out = a AND b / a OR b / a AND NOT b over n chunks. */
+int ndx_chunks_and(const uint32_t* d_a, const uint32_t* d_b, uint32_t* d_out, uint64_t n,
+                   void* stream);
+int ndx_chunks_or(const uint32_t* d_a, const uint32_t* d_b, uint32_t* d_out, uint64_t n,
+                  void* stream);
+int ndx_chunks_andnot(const uint32_t* d_a, const uint32_t* d_b, uint32_t* d_out, uint64_t n,
+                      void* stream);
+/* rows_for (wah_words.cpp:93-103) on a decoded bitmap: the rows of the set
+ * bits below row_limit, ascending; *d_count = their number.  d_rows must
+ * hold every set bit of the chunks. */
+size_t ndx_chunks_rows_scratch_bytes(uint64_t n_chunks);
+int ndx_chunks_rows(const uint32_t* d_chunks, uint64_t n_chunks, uint32_t row_limit,
+                    uint32_t* d_rows, void* d_scratch, uint32_t* d_count, void* stream);
+/* Canonical words of a chunk array (CanonicalWriter, wah.hpp:36-74): every
+ * chunk (trim_trailing = 0, as encode() does) or up to the last set bit
+ * (trim_trailing = 1, as an index bitmap).  d_words holds up to n_chunks
+ * words; d_info[0] = word count, [1] error flags, [2] chunks encoded. */
+size_t ndx_wah_encode_scratch_bytes(uint64_t n_chunks);
+int ndx_wah_encode(const uint32_t* d_chunks, uint64_t n_chunks, int trim_trailing,
+                   uint32_t* d_words, void* d_scratch, uint32_t* d_info, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Multi-GPU build: shards of rows [S_g, S_{g+1}),
  * S_g = 0 mod 31, are built with row_base = S_g; the pieces are then merged.
  * ------------------------------------------------------------------------- */

@@ -62,6 +62,15 @@ SIGNATURES = [
     ("ndx_wah_emit", ctypes.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ndx_wah_table", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_wah_copy_out", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u64, _vp]),
+    ("ndx_wah_decode_scratch_bytes", _sz, [_u64]),
+    ("ndx_wah_decode", ctypes.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
+    ("ndx_chunks_and", ctypes.c_int, [_vp, _vp, _vp, _u64, _vp]),
+    ("ndx_chunks_or", ctypes.c_int, [_vp, _vp, _vp, _u64, _vp]),
+    ("ndx_chunks_andnot", ctypes.c_int, [_vp, _vp, _vp, _u64, _vp]),
+    ("ndx_chunks_rows_scratch_bytes", _sz, [_u64]),
+    ("ndx_chunks_rows", ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp]),
+    ("ndx_wah_encode_scratch_bytes", _sz, [_u64]),
+    ("ndx_wah_encode", ctypes.c_int, [_vp, _u64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("ndx_wah_shard_meta", ctypes.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_wah_assemble", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     ("ndx_scan_scratch_bytes", _sz, [_u64]),

@@ -140,3 +140,14 @@ def test_merge_plan_padded_input_equals_concatenated(port):
     e2, p2, w2 = shard.plan_merge(pad, [m.size for m in metas])
     assert w1 == w2 and np.array_equal(e1, e2)
     assert all(np.array_equal(a, b_) for a, b_ in zip(p1, p2))
+
+
+def test_query_chunk_helpers_round_trip():
+    from paper_1709_07781_b200 import query
+
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 30, 31, 32, 100, 1000):
+        b = rng.random(n) < 0.3
+        c = query.bits_to_chunks(b)
+        assert c.size == (n + 30) // 31 and (c < (1 << 31)).all()
+        assert np.array_equal(query.chunks_to_bits(c, n), b)
