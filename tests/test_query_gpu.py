@@ -66,3 +66,22 @@ def test_bitmap_algebra_over_the_index(builder, port, op):
         last = np.nonzero(want)[0]
         ref = port.encode(want[: last[-1] + 1].astype(np.uint8)) if last.size else np.zeros(0, np.uint32)
         assert np.array_equal(idx.combine(op, a, b), ref), (op, a, b)
+
+
+def test_cli_index_file_is_the_reference_index(tmp_path, port):
+    """p/tests/test_cli.cpp:61-80: `--seed 5 index build --rows 3000
+    --cardinality 7 --verify --output f` writes the reference index byte for
+    byte."""
+    import oracle
+    from paper_1709_07781_b200 import cli
+
+    out = tmp_path / "cli_index.wah"
+    assert cli.main(["index", "build", "--seed", "5", "--rows", "3000", "--cardinality", "7", "--verify",
+                     "--output", str(out)]) == 0
+    v = gen.uniform(5, 3000, 7)
+    assert out.read_bytes() == port.reference_index(v).serialize()
+    raw = tmp_path / "vals.raw"
+    v.astype("<u4").tofile(raw)
+    out2 = tmp_path / "from_raw.wah"
+    assert cli.main(["index", "build", "--input", str(raw), "--verify", "--output", str(out2)]) == 0
+    assert out2.read_bytes() == out.read_bytes()
