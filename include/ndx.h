@@ -217,6 +217,12 @@ int ndx_compact_move(uint32_t* d_cfg, const uint32_t* d_data, uint64_t n,
                      const uint32_t* d_counts, uint32_t* d_out,
                      void* d_scratch, void* stream);
 
+/* out = a x b for n x n row-major fp32 matrices, the k sum in ascending order
+ * with separately rounded multiply and add (bit-identical to the reference's
+ * triple loop): the matmul actor of the paper's facade-overhead protocol
+ * (p/core/src/bench_protocols.cpp, acceptance.cpp checks 6-7). */
+int ndx_matmul_f32(const float* d_a, const float* d_b, float* d_out, uint64_t n, void* stream);
+
 /* One-CTA, one-warp `p[0] += 1` kernel: the dispatch-overhead probe of
  * BASELINE config 2 (p/benchmarks/bench_device.cpp:14-24). */
 int ndx_tiny_increment(uint32_t* d_p, void* stream);

@@ -313,3 +313,42 @@ int ndx_wah_encode(const uint32_t* d_chunks, uint64_t n_chunks, int trim_trailin
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// fp32 square matrix product for the paper's facade-overhead protocol
+// (p/core/src/bench_protocols.cpp spawn_matmul / enqueue_matmul): one output
+// per thread, the k sum in ascending order with separately rounded multiply
+// and add, so the result is bit-identical to the triple-loop oracle.  It is
+// a dispatch-overhead probe at n <= 256, not a GEMM workload.
+namespace ndx {
+namespace {
+constexpr int kMmTile = 16;
+__global__ void k_matmul(const float* __restrict__ a, const float* __restrict__ b,
+                         float* __restrict__ out, uint32_t n) {
+  __shared__ float ta[kMmTile][kMmTile], tb[kMmTile][kMmTile + 1];
+  const uint32_t x = blockIdx.x * kMmTile + threadIdx.x, y = blockIdx.y * kMmTile + threadIdx.y;
+  float acc = 0.f;
+  for (uint32_t k0 = 0; k0 < n; k0 += kMmTile) {
+    const uint32_t ka = k0 + threadIdx.x, kb = k0 + threadIdx.y;
+    ta[threadIdx.y][threadIdx.x] = (y < n && ka < n) ? a[uint64_t(y) * n + ka] : 0.f;
+    tb[threadIdx.y][threadIdx.x] = (kb < n && x < n) ? b[uint64_t(kb) * n + x] : 0.f;
+    __syncthreads();
+    const uint32_t kmax = umin<uint32_t>(kMmTile, n - k0);
+    for (uint32_t k = 0; k < kmax; ++k) acc = __fadd_rn(acc, __fmul_rn(ta[threadIdx.y][k], tb[k][threadIdx.x]));
+    __syncthreads();
+  }
+  if (x < n && y < n) out[uint64_t(y) * n + x] = acc;
+}
+}  // namespace
+}  // namespace ndx
+
+extern "C" int ndx_matmul_f32(const float* d_a, const float* d_b, float* d_out, uint64_t n,
+                              void* stream) {
+  if (n == 0) return 0;
+  if (!d_a || !d_b || !d_out) return NDX_E_INVALID;
+  if (n > 65536) return NDX_E_TOO_LARGE;
+  const dim3 block(ndx::kMmTile, ndx::kMmTile);
+  const dim3 grid(unsigned((n + ndx::kMmTile - 1) / ndx::kMmTile), unsigned((n + ndx::kMmTile - 1) / ndx::kMmTile));
+  ndx::k_matmul<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(d_a, d_b, d_out, uint32_t(n));
+  return cudaGetLastError();
+}

@@ -554,6 +554,58 @@ Event Device::enqueue_write_bytes(const Buffer& b, std::vector<std::byte> data,
   return submit(impl_, std::move(w), deps);
 }
 
+Event Device::enqueue_write_from(const Buffer& b, const void* src, std::size_t bytes,
+                                 std::vector<Event> deps) {
+  check_target(this, b);
+  check_deps(deps);
+  if (bytes != b.bytes()) throw DeviceError("write size does not match the buffer");
+  if (!src && bytes) throw DeviceError("write source is null");
+  auto st = b.shared_state();
+  Issue w{"write", [st, src, bytes](void* s) -> int {
+            if (st->freed.load()) return NDX_E_INVALID;
+            return bytes ? ndx_memcpy_h2d_async(st->ptr, src, bytes, s) : 0;
+          }, {}};
+  return submit(impl_, std::move(w), deps);
+}
+
+Event Device::enqueue_read_into(const Buffer& b, void* dst, std::size_t nbytes, std::vector<Event> deps) {
+  if (!dst && nbytes) throw DeviceError("read destination is null");
+  return enqueue_read_with(
+      b, nbytes, [dst](const void* p, std::size_t k) { if (k) std::memcpy(dst, p, k); }, std::move(deps));
+}
+
+Event Device::enqueue_read_with(const Buffer& b, std::size_t nbytes,
+                                std::function<void(const void*, std::size_t)> consume,
+                                std::vector<Event> deps) {
+  check_target(this, b);
+  check_deps(deps);
+  if (nbytes > b.bytes()) throw DeviceError("read size exceeds the buffer");
+  auto st = b.shared_state();
+  auto d = impl_;
+  struct Stage {
+    void* pinned = nullptr;
+    std::size_t cap = 0;
+  };
+  auto stage = std::make_shared<Stage>();
+  stage->pinned = d->pinned_get(std::max<std::size_t>(nbytes, 1), stage->cap);
+  if (!stage->pinned) throw DeviceError("cannot allocate pinned staging memory");
+  Issue w{"read", [st, stage, nbytes](void* s) -> int {
+            if (st->freed.load()) return NDX_E_INVALID;
+            return nbytes ? ndx_memcpy_d2h_async(stage->pinned, st->ptr, nbytes, s) : 0;
+          }, {}};
+  Event ev = detail::make_device_event(d);
+  ev.shared_state()->before_complete = [d, stage, nbytes, consume = std::move(consume)] {
+    consume(stage->pinned, nbytes);
+    d->pinned_put(stage->pinned, stage->cap);
+  };
+  Event issued = submit(d, std::move(w), deps);
+  auto es = ev.shared_state();
+  issued.add_callback([es, issued](EventState s) {
+    detail::finish_event(es, s == EventState::complete, s == EventState::complete ? "" : issued.error());
+  });
+  return ev;
+}
+
 Event Device::enqueue_read_bytes(const Buffer& b, std::shared_ptr<std::vector<std::byte>> dst,
                                  std::vector<Event> deps) {
   check_target(this, b);

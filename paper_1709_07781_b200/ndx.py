@@ -81,6 +81,7 @@ SIGNATURES = [
     ("ndx_compact_count", ctypes.c_int, [_vp, _u64, _vp, _vp]),
     ("ndx_compact_move_scratch_bytes", _sz, [_u64]),
     ("ndx_compact_move", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    ("ndx_matmul_f32", ctypes.c_int, [_vp, _vp, _vp, _u64, _vp]),
     ("ndx_tiny_increment", ctypes.c_int, [_vp, _vp]),
 ]
 
