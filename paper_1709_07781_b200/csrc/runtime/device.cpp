@@ -337,6 +337,11 @@ void issue_now(const std::shared_ptr<DeviceImpl>& d, const Event& ev, Issue& w) 
   for (const Event& dep : w.other_device) {
     auto od = dep.shared_state()->dev.lock();
     if (!od) continue;
+    // the dependency may still sit in the other device's launch ring: the
+    // fence must follow its actual launch
+    const std::uint64_t want = dep.shared_state()->seq.load(std::memory_order_acquire);
+    for (unsigned i = 0; od->launched.load(std::memory_order_acquire) < want; ++i)
+      if (i > 256) std::this_thread::yield();
     void* fence = nullptr;
     if (ndx_event_create(&fence, 0) == 0) {
       ndx_event_record(fence, od->stream);  // after the dependency on its stream

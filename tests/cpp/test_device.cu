@@ -598,3 +598,38 @@ TEST("gpu", "wah: index file round trip of a device-built index") {
   wah::write_index_file(path, idx);
   CHECK(wah::read_index_file(path) == idx);
 }
+
+TEST("gpu", "multi-device: copy_to moves references between devices; foreign refs are a mismatch") {
+  // two Devices (own streams, own actors); on a one-GPU box both use ordinal 0
+  int count = 0;
+  cudaGetDeviceCount(&count);
+  ActorSystem sys(2);
+  Device a(DeviceConfig{0}), b(DeviceConfig{count > 1 ? 1 : 0});
+  ComputeActorSpec spec;
+  spec.kernel = KernelDef("double_in_place", LAUNCHER(k_times2_inplace<<<g3(lp), b3(lp), 0, (cudaStream_t)lp.stream>>>((uint32_t*)lp.ptr[0], lp.len[0])));
+  spec.range = NdRange::linear(4);
+  spec.args = {ArgSpec::in_out(ElemType::u32, ArgMode::ref, ArgMode::ref)};
+  auto on_a = spawn_compute(sys, a, spec);
+  auto on_b = spawn_compute(sys, b, spec);
+  Buffer buf = a.create_buffer(ElemType::u32, 4);
+  MemRef ref(buf, a.enqueue_write(buf, std::vector<uint32_t>{1, 2, 3, 4}));
+  Reply r1 = sys.request(on_a, Message::of(ref)).await();
+  REQUIRE(!is_error(r1));
+  MemRef ra = get_message(r1).at(0).as_ref();
+  // a reference of device a is not accepted by an actor on device b
+  Reply bad = sys.request(on_b, Message::of(ra)).await();
+  REQUIRE(is_error(bad));
+  CHECK(get_error(bad).code == ErrorCode::mismatch);
+  MemRef rb = copy_to(ra, b);
+  CHECK(&rb.buffer().device() == &b);
+  Reply r2 = sys.request(on_b, Message::of(rb)).await();
+  REQUIRE(!is_error(r2));
+  CHECK((retrieve_u32(get_message(r2).at(0).as_ref()) == std::vector<uint32_t>{4, 8, 12, 16}));
+  CHECK((retrieve_u32(ra) == std::vector<uint32_t>{2, 4, 6, 8}));  // the source is untouched
+  get_message(r2).at(0).as_ref().release();
+  ra.release();
+  settle(sys, a);
+  settle(sys, b);
+  CHECK(a.live_buffers() == 0);
+  CHECK(b.live_buffers() == 0);
+}
