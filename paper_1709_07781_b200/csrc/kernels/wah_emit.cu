@@ -357,6 +357,18 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
     const bool full = has && by_bulk(tile);
     const uint64_t* B = buf0 + b * kEmitBuf + kHaloL;  // B[li] = pairs[tile * kEmitTile + li]
     const uint32_t ts = tile * kEmitTile, li0 = threadIdx.x * kEmitK;
+    // Start the reads of the aggregates the previous tile's write-out needs
+    // now, so their latency hides behind phase 1 (most are published by now;
+    // the few that are not get re-read after phase 1).
+    constexpr int kAggPre = 4;
+    uint64_t pre[kAggPre];
+    const uint64_t agg_lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
+    const uint64_t agg_hi = pending < 0 ? agg_lo : uint64_t(pending);
+#pragma unroll
+    for (int j = 0; j < kAggPre; ++j) {
+      const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
+      pre[j] = a < agg_hi ? ld_relaxed_u64(&agg[a]) : kAggReady;
+    }
     if (has) {
       if (full) {
         mbar_wait(&bar[b], (phase >> b) & 1u);
@@ -408,9 +420,20 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       // ---- write the previous tile out: global offsets first
       const int pb = b ^ 1;
       const uint64_t pt = uint64_t(pending);
-      const uint64_t lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
       uint32_t sw = 0, sd = 0;
-      for (uint64_t j = lo + threadIdx.x; j < pt; j += kEmitThreads) {
+#pragma unroll
+      for (int j = 0; j < kAggPre; ++j) {
+        const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
+        if (a >= pt) break;
+        uint64_t s = pre[j];
+        while (!(s & kAggReady)) {
+          __nanosleep(32);
+          s = ld_relaxed_u64(&agg[a]);
+        }
+        sw += uint32_t(s);
+        sd += uint32_t(s >> 32) & 0x7fffffffu;
+      }
+      for (uint64_t j = agg_lo + threadIdx.x + uint64_t(kAggPre) * kEmitThreads; j < pt; j += kEmitThreads) {
         uint64_t s = ld_relaxed_u64(&agg[j]);
         while (!(s & kAggReady)) {
           __nanosleep(32);
