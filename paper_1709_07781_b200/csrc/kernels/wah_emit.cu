@@ -388,17 +388,23 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       }
       // literal carried into each span: segmented OR-scan over the spans'
       // trailing ORs (bit 31 = the span holds a run head)
+      // ... and, interleaved with it (two independent shuffle chains), the
+      // inclusive sum of the spans' (words << 16 | value heads)
       uint32_t x = (sp.hmask ? 0x80000000u : 0u) | sp.acc;
+      const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
+      uint32_t incl = cnt;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t y = __shfl_up_sync(kFull, x, d);
-        if (lane >= d && !(x >> 31)) x |= y;
+        const uint32_t z = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) {
+          if (!(x >> 31)) x |= y;
+          incl += z;
+        }
       }
       const uint32_t incl_lit = (x & kLiteralMask) | ((x >> 31) ? 0u : wcarry);
       carry_in = __shfl_up_sync(kFull, incl_lit, 1);
       if (lane == 0) carry_in = wcarry;
-      const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
-      const uint32_t incl = warp_incl_sum(cnt);
       excl = incl - cnt;
       if (lane == 31) s_wt[b][warp] = incl;
     }
