@@ -67,6 +67,14 @@ namespace ndx {
 #ifndef NDX_SORT_NARROW_B
 #define NDX_SORT_NARROW_B 0
 #endif
+// issue the first look-back read before the staging: measured -1% on the
+// byte passes, +2% on the wide pass (more spills there)
+#ifndef NDX_SORT_EARLY_LB_B
+#define NDX_SORT_EARLY_LB_B 1
+#endif
+#ifndef NDX_SORT_EARLY_LB_W
+#define NDX_SORT_EARLY_LB_W 0
+#endif
 #ifndef NDX_SORT_ATOMRANK
 #define NDX_SORT_ATOMRANK 0
 #endif
@@ -443,6 +451,19 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* st, uint64_t tile, 
   return excl;
 }
 
+// The same, with the status of tile-1 already loaded (`s0`).
+__device__ __forceinline__ uint64_t lookback_from(const uint64_t* st, uint64_t tile, uint32_t nb,
+                                                  uint32_t d, uint32_t epoch, uint64_t s0) {
+  const uint64_t* p0 = &st[(tile - 1) * nb + d];
+  while (!st_ready(s0, epoch)) {
+    __nanosleep(64);
+    s0 = ld_relaxed_u64(p0);
+  }
+  uint64_t excl = s0 & kStValue;
+  if ((s0 & (3ull << 38)) == kStPrefix || tile == 1) return excl;
+  return excl + lookback(st, tile - 1, nb, d, epoch);
+}
+
 // One tile of a stable scatter pass.  BITS is the digit width (compile
 // time, so the ballot match unrolls straight); FULL tiles skip every bounds
 // check.  Element order within a warp is round-major / lane-minor, which is
@@ -562,6 +583,55 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
 #endif
   block_excl_scan(t.cnt, t.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
 
+  if constexpr (SH::kWide ? NDX_SORT_EARLY_LB_W : NDX_SORT_EARLY_LB_B) {
+  // ---- look-back, part 1: the first predecessor status of each of this
+  // thread's digits is requested now; its round trip overlaps the rank
+  // adjustment and the staging, which only need tile-local offsets
+  constexpr int ND = int((NB + SH::THREADS - 1) / SH::THREADS);
+  uint64_t first[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    const uint32_t d = threadIdx.x + uint32_t(k) * SH::THREADS;
+    first[k] = (tile > 0 && d < NB) ? ld_relaxed_u64(&t.status[(tile - 1) * NB + d]) : 0ull;
+    if (d < NB) {
+      const uint32_t local = t.gbase[d];
+#pragma unroll
+      for (int w = 0; w < SH::WARPS; ++w) t.H[w * NBMAX + d] += uint16_t(local);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < SH::IPT; ++r) {
+    const uint32_t d = digit(key[r]);
+    if (NARROW)
+      key[r] += uint32_t(Hw[d]) << 16;
+    else
+      rank[r] += Hw[d];
+  }
+  __syncthreads();  // H no longer read: S may overwrite it
+#pragma unroll
+  for (int r = 0; r < SH::IPT; ++r)
+    if (FULL || wofs + r * 32 < tile_n) {
+      if (NARROW)
+        t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay[r]) << 32);
+      else
+        t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+    }
+  // ---- look-back, part 2: finish from the status already in hand
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    const uint32_t d = threadIdx.x + uint32_t(k) * SH::THREADS;
+    if (d >= NB) break;
+    const uint32_t c = t.cnt[d], local = t.gbase[d];
+    uint64_t excl = 0;
+    if (tile > 0) {
+      excl = lookback_from(t.status, tile, NB, d, t.epoch, first[k]);
+      st_relaxed_u64(&st[d], st_word(t.epoch, kStPrefix, excl + c));
+    }
+    t.gbase[d] = t.bstart[d] + uint32_t(excl) - local;
+  }
+  __syncthreads();
+  } else {
   // ---- look-back: global base of each digit for this tile
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
     const uint32_t c = t.cnt[d], local = t.gbase[d];
@@ -595,6 +665,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
         t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
     }
   __syncthreads();
+  }
 
   // ---- scatter: consecutive local slots of one digit are consecutive globally
   const uint32_t lim = FULL ? uint32_t(SH::TILE) : tile_n;
