@@ -182,3 +182,19 @@ def test_row_base_shards(builder, port, k_chunks):
     got = builder.build(v, row_base=31 * k_chunks)
     ents, words = _shift_index(port.reference_index(v), k_chunks)
     assert np.array_equal(got.entries, ents) and np.array_equal(got.words, words)
+
+
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 2048 * 3 + 31, 8191, 8192, 8193, 16383, 16384, 16385,
+                               16384 * 3 + 1, 4096 * 37])
+@pytest.mark.parametrize("kind", ["uniform", "clustered", "zipf"])
+def test_tile_boundaries(builder, port, n, kind):
+    """Sizes around the emit tile (2048 pairs), the byte-pass tile (8192)
+    and the wide-pass tile (16384), with short and long runs."""
+    rng = np.random.default_rng(n)
+    if kind == "uniform":
+        v = rng.integers(0, 3000, n).astype(np.uint32)
+    elif kind == "clustered":
+        v = np.repeat(rng.integers(0, 5, (n + 99) // 100), 100)[:n].astype(np.uint32)
+    else:
+        v = gen.zipf(n, n, 70000, 1.0)
+    assert same(builder.build(v), port.reference_index(v)), (n, kind)
