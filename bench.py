@@ -288,6 +288,44 @@ def run_sharded(args, cfg, world, rank, local):
     return 0
 
 
+def extra_config(rt, raw, dev, K, W_, name="C3"):
+    """BASELINE config 3 beside the headline: 2^26 uniform values over 1024
+    keys through the same 4-stage actor chain (device-resident keys, CUDA
+    events on the runtime stream) plus its per-stage times."""
+    import torch
+
+    c = CONFIGS[name]
+    n = c["n"]
+    keys = torch.from_numpy(gen_values(c, n, 0).view(np.int32)).to(dev)
+    rts = torch.cuda.ExternalStream(rt.stream, device=dev)
+    for _ in range(W_):
+        rt.build_index_device(keys.data_ptr(), n)
+    rt.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(rts)
+    for _ in range(K):
+        rt.build_index_device(keys.data_ptr(), n)
+    a1.record(rts)
+    a1.synchronize()
+    ms = a0.elapsed_time(a1) / K
+    stream = torch.cuda.current_stream()
+    calls = raw.stage_calls(keys, n, row_base=0, stream=stream)
+    for _, cl in calls:
+        cl()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(K)]
+    for k in range(K):
+        ev[k][0].record(stream)
+        for i, (_, cl) in enumerate(calls):
+            cl()
+            ev[k][i + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    stage_ms = {nm: sum(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(K)) / K
+                for i, (nm, _) in enumerate(calls)}
+    W, D = raw.counts()
+    return {"workload": c["desc"], "value": n / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "stage_ms": stage_ms, "words": W, "distinct": D, "data": "synthetic (mt19937(1), uniform)"}
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -450,6 +488,8 @@ def run_ours(args, cfg):
         "gpu_launches": 11 * K,
         "clocks": clk,
     }
+    if world == 1 and args.config == "C4" and not args.no_extra:
+        line["other_configs"] = {"C3": extra_config(rt, raw, dev, K, W_)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
@@ -473,6 +513,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3 line inside the C4 report")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU step (shard meta, all-gather, merge) even at N=1")
     args = ap.parse_args()
