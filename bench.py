@@ -208,9 +208,10 @@ def run_sharded(args, cfg, world, rank, local):
 
     def step(k):
         W, D, meta_d = sb.build(k, n_r, base)
-        metas, sizes = shard.exchange_meta_device(meta_d, D)
-        entries, pieces, total = shard.plan_merge(metas, sizes)
-        state.update(W=W, D=D, entries=entries, pieces=pieces, total=total)
+        padded, sizes = shard.exchange_meta_device(meta_d, D)
+        entries, pieces, nent, total = shard.plan_merge_device(padded, sizes)
+        state.update(W=W, D=D, entries=entries, pieces=pieces, total=total, nent=nent,
+                     cap=padded.shape[1] // 8, sizes=sizes)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -247,7 +248,7 @@ def run_sharded(args, cfg, world, rank, local):
     g0 = time.perf_counter()
     staged = shard.gather_words(sb.words[: state["W"]], dst=0)
     if rank == 0:
-        shard.assemble(staged, state["pieces"], state["total"], dev, out=out)
+        shard.assemble_slots(staged, state["pieces"], state["cap"], state["sizes"], state["total"], out=out)
     barrier()
     gather_ms = max_over_ranks((time.perf_counter() - g0) * 1e3)
 
@@ -272,10 +273,11 @@ def run_sharded(args, cfg, world, rank, local):
                    "l2": "inputs larger than L2 (4 B keys x values per GPU > 126 MB)",
                    "parallelism": f"row shards x{world} (31-aligned), NCCL metadata all-gather, "
                                   f"boundary merge (SURVEY App. B)",
-                   "words": state["total"], "distinct": int(len(state["entries"])),
+                   "words": state["total"], "distinct": state["nent"],
                    "path": "per-rank 4-stage build (global row ids) + shard metadata kernel + NCCL "
-                           "all-gather of the metadata + merge plan (every rank knows where each of "
-                           "its words goes); the gather of all words to rank 0 is timed separately"},
+                           "all-gather of the metadata + merge plan on the GPU (every rank knows where "
+                           "each of its words goes); the gather of all words to rank 0 is timed "
+                           "separately"},
         "gather_to_rank0_ms": gather_ms,
         "e2e": {"value": total_values / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
                 "d2h_bytes_per_step": 4 * state["W"], "ms_per_step": e2e_ms},

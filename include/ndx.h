@@ -185,6 +185,19 @@ typedef struct {
 int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
                        uint64_t n_entries, const uint32_t* d_words, ndx_shard_meta* d_meta,
                        void* stream);
+/* The merge plan on the device (same result as ndactor_merge_plan): shard
+ * g's records at d_metas + g*stride, h_counts[g] of them (host array,
+ * shards <= 64).  Writes the merged (value, offset, length) entries and one
+ * ndx_piece per record at the same slot (dst absolute).  d_totals: [0]
+ * entries, [1] words, [2] error flags (1 empty body, 2 overlapping shards). */
+size_t ndx_merge_plan_scratch_bytes(uint64_t records);
+int ndx_merge_plan(const ndx_shard_meta* d_metas, uint64_t stride, const uint64_t* h_counts,
+                   uint32_t shards, uint32_t* d_entries, ndx_piece* d_pieces, uint64_t* d_totals,
+                   void* d_scratch, void* stream);
+/* Copies every piece of a device plan (slots g*stride + i, h_counts[g] per
+ * shard) to out; h_src[g] is shard g's words (device pointers, host array). */
+int ndx_wah_assemble_slots(const uint32_t* const* h_src, uint32_t shards, const ndx_piece* d_pieces,
+                           uint64_t stride, const uint64_t* h_counts, uint32_t* d_out, void* stream);
 /* Copies every piece to out (the merged words). */
 int ndx_wah_assemble(const uint32_t* d_src, const ndx_piece* d_pieces, uint64_t n_pieces,
                      uint32_t* d_out, void* stream);

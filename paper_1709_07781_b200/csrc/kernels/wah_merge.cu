@@ -8,9 +8,9 @@
 //   * the local leading zero-fill is replaced by the cross-shard gap fill
 //     (or dropped / kept for the first piece),
 //   * ones-fills that meet at gap 0 are fused into one.
-// The planning over the (small) metadata runs on the host
-// (csrc/runtime/merge_plan.cpp); these kernels do the per-value metadata and
-// the copy of every piece to its final position.
+// The planning over the (small) metadata runs on the device (wah_plan.cu)
+// or on the host (csrc/runtime/wah_shard.cpp); these kernels do the
+// per-value metadata and the copy of every piece to its final position.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -107,3 +107,53 @@ int ndx_wah_assemble(const uint32_t* d_src, const ndx_piece* d_pieces, uint64_t 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Assembly straight from the device plan: pieces in their plan slots
+// (g * stride + i), every shard's words in its own buffer.  One CTA per
+// piece, the CTA striding over the piece's words (a hot value's piece spans
+// millions of words).
+namespace ndx {
+namespace {
+constexpr int kAsmShards = 64;
+struct ShardSrc {
+  const uint32_t* src[kAsmShards];
+  uint32_t count[kAsmShards];
+};
+__global__ void __launch_bounds__(512) k_assemble_slots(ShardSrc ss, uint32_t shards, uint32_t stride,
+                                                        const ndx_piece* __restrict__ pieces,
+                                                        uint32_t* __restrict__ out) {
+  const uint64_t slots = uint64_t(shards) * stride;
+  for (uint64_t x = blockIdx.x; x < slots; x += gridDim.x) {
+    const uint32_t g = uint32_t(x / stride), i = uint32_t(x % stride);
+    if (i >= ss.count[g]) continue;
+    const ndx_piece pc = pieces[x];
+    uint32_t* dst = out + pc.dst;
+    if (pc.lead) {
+      if (threadIdx.x == 0) dst[0] = pc.lead;
+      ++dst;
+    }
+    const uint32_t* s = ss.src[g] + pc.src_off;
+    for (uint32_t j = threadIdx.x; j < pc.src_len; j += blockDim.x) dst[j] = __ldg(s + j);
+  }
+}
+}  // namespace
+}  // namespace ndx
+
+extern "C" int ndx_wah_assemble_slots(const uint32_t* const* h_src, uint32_t shards,
+                                      const ndx_piece* d_pieces, uint64_t stride,
+                                      const uint64_t* h_counts, uint32_t* d_out, void* stream) {
+  if (!h_src || !d_pieces || !h_counts || !d_out || shards == 0 || shards > 64) return NDX_E_INVALID;
+  ndx::ShardSrc ss{};
+  uint64_t total = 0;
+  for (uint32_t g = 0; g < shards; ++g) {
+    ss.src[g] = h_src[g];
+    ss.count[g] = uint32_t(h_counts[g]);
+    total += h_counts[g];
+  }
+  if (total == 0) return 0;
+  const int grid = int(umin<uint64_t>(uint64_t(shards) * stride, 148ull * 32));
+  ndx::k_assemble_slots<<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(ss, shards, uint32_t(stride),
+                                                                             d_pieces, d_out);
+  return cudaGetLastError();
+}

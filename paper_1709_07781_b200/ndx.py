@@ -72,6 +72,9 @@ SIGNATURES = [
     ("ndx_wah_encode_scratch_bytes", _sz, [_u64]),
     ("ndx_wah_encode", ctypes.c_int, [_vp, _u64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("ndx_wah_shard_meta", ctypes.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
+    ("ndx_merge_plan_scratch_bytes", _sz, [_u64]),
+    ("ndx_merge_plan", ctypes.c_int, [_vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
+    ("ndx_wah_assemble_slots", ctypes.c_int, [_vp, _u32, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_wah_assemble", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     ("ndx_scan_scratch_bytes", _sz, [_u64]),
     ("ndx_scan_exclusive_u32", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),

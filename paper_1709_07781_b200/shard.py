@@ -116,9 +116,10 @@ def exchange_meta(meta: np.ndarray, group=None) -> list[np.ndarray]:
 
 def exchange_meta_device(meta_d, D: int, group=None):
     """All-gather of device-resident metadata (meta_d: int32 tensor of at
-    least D*8 words on this rank's GPU) over NCCL, one copy to the host.
-    Returns (padded (G, cap) META_DTYPE array, per-rank record counts) --
-    the form plan_merge takes without copying."""
+    least D*8 words on this rank's GPU) over NCCL.  Returns (a (G, cap*8)
+    int32 device tensor of the padded records, per-rank record counts): the
+    input of plan_merge_device; `host_metas` turns it into the (G, cap)
+    META_DTYPE array plan_merge takes."""
     import torch
     import torch.distributed as dist
     ws = dist.get_world_size(group)
@@ -135,8 +136,54 @@ def exchange_meta_device(meta_d, D: int, group=None):
         mine[: D * 8] = meta_d[: D * 8]
     out = torch.empty(ws * cap * 8, dtype=torch.int32, device=dev)
     dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
-    host = out.cpu().numpy().view(META_DTYPE).reshape(ws, cap)
-    return host, sizes
+    return out.view(ws, cap * 8), sizes
+
+
+def host_metas(padded) -> np.ndarray:
+    g = padded.shape[0]
+    return padded.cpu().numpy().view(META_DTYPE).reshape(g, -1)
+
+
+def plan_merge_device(padded, sizes):
+    """The merge plan on the GPU (ndx_merge_plan), same result as plan_merge.
+    padded: (G, cap*8) int32 device tensor; returns (entries (D,3) int32
+    device tensor, pieces (G*cap*24 bytes) device tensor, D, W)."""
+    import torch
+    from . import ndx
+    lib = ndx.load()
+    G, cap8 = padded.shape
+    cap = cap8 // 8
+    counts = np.asarray(sizes, np.uint64)
+    dev = padded.device
+    rec = int(counts.sum())
+    entries = torch.empty(max(rec, 1) * 3, dtype=torch.int32, device=dev)
+    pieces = torch.empty(max(G * cap, 1) * 6, dtype=torch.int32, device=dev)
+    totals = torch.zeros(3, dtype=torch.int64, device=dev)
+    scr = torch.empty(lib.ndx_merge_plan_scratch_bytes(rec) // 4 + 64, dtype=torch.int32, device=dev)
+    ndx.check(lib.ndx_merge_plan(ndx._ptr(padded), cap, counts.ctypes.data, G, ndx._ptr(entries), ndx._ptr(pieces),
+                                 ndx._ptr(totals), ndx._ptr(scr), torch.cuda.current_stream(dev).cuda_stream),
+              "merge_plan")
+    t = totals.cpu().numpy()
+    if t[2]:
+        raise RuntimeError("merge plan: inconsistent shard metadata (flags %d)" % int(t[2]))
+    D, W = int(t[0]), int(t[1])
+    return entries[: 3 * D].view(D, 3), pieces, D, W
+
+
+def assemble_slots(staged: list, pieces, cap: int, sizes, total_words: int, out=None):
+    """Assemble from a device plan: staged[g] = shard g's words (device)."""
+    import torch
+    from . import ndx
+    lib = ndx.load()
+    dev = pieces.device
+    if out is None:
+        out = torch.empty(max(total_words, 1), dtype=torch.int32, device=dev)
+    srcs = (ctypes.c_void_p * len(staged))(*[s.data_ptr() for s in staged])
+    counts = np.asarray(sizes, np.uint64)
+    ndx.check(lib.ndx_wah_assemble_slots(srcs, len(staged), ndx._ptr(pieces), cap, counts.ctypes.data,
+                                         ndx._ptr(out), torch.cuda.current_stream(dev).cuda_stream),
+              "assemble_slots")
+    return out[:total_words]
 
 
 def gather_words(words, dst: int = 0, group=None):
@@ -259,9 +306,10 @@ def build_distributed(values_local: np.ndarray, row_base: int, builder: ShardBui
     keys = torch.from_numpy(np.ascontiguousarray(values_local, np.uint32).view(np.int32)).to(dev)
     n = keys.numel()
     W, D, meta_d = builder.build(keys, n, row_base)
-    metas, sizes = exchange_meta_device(meta_d, D, group)
-    entries, pieces, total = plan_merge(metas, sizes)
+    padded, sizes = exchange_meta_device(meta_d, D, group)
+    entries, pieces, _, total = plan_merge_device(padded, sizes)
     staged = gather_words(builder.words[:W], dst=0, group=group)
+    ent = entries.cpu().numpy().view(np.uint32)
     if dist.get_rank(group) != 0:
-        return entries, None
-    return entries, assemble(staged, pieces, total, dev)
+        return ent, None
+    return ent, assemble_slots(staged, pieces, padded.shape[1] // 8, sizes, total)

@@ -28,6 +28,16 @@ def _sharded_build(v: np.ndarray, g: int):
         staged.append(sb.words[:W].clone())
     entries, pieces, total = shard.plan_merge(metas)
     words = shard.assemble(staged, pieces, total, torch.device("cuda"))
+    # the device planner from the same metadata, padded as the all-gather delivers it
+    cap = max([m.size for m in metas] + [1])
+    pad = np.zeros((g, cap), shard.META_DTYPE)
+    for k, m in enumerate(metas):
+        pad[k, :m.size] = m
+    dpad = torch.from_numpy(pad.view(np.int32).reshape(g, cap * 8).copy()).cuda()
+    d_ent, d_pieces, nent, total2 = shard.plan_merge_device(dpad, [m.size for m in metas])
+    assert total2 == total and np.array_equal(d_ent.cpu().numpy().view(np.uint32), entries)
+    words2 = shard.assemble_slots(staged, d_pieces, cap, [m.size for m in metas], total2)
+    assert np.array_equal(words2.cpu().numpy(), words.cpu().numpy())
     return entries, words.cpu().numpy().view(np.uint32)
 
 

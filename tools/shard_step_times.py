@@ -25,13 +25,13 @@ for it in range(4):
     W, D, meta_d = sb.build(keys, n, 0)
     torch.cuda.synchronize(); t.append(time.perf_counter())
     t.append(time.perf_counter())
-    metas, sizes = shard.exchange_meta_device(meta_d, D)
+    padded, sizes = shard.exchange_meta_device(meta_d, D)
     t.append(time.perf_counter())
-    entries, pieces, total = shard.plan_merge(metas, sizes)
+    entries, pieces, nent, total = shard.plan_merge_device(padded, sizes)
     t.append(time.perf_counter())
     if out is None:
         out = torch.empty(total, dtype=torch.int32, device="cuda")
-    shard.assemble([sb.words[:W]], [pieces[0]], total, torch.device("cuda"), out=out)
+    shard.assemble_slots([sb.words[:W]], pieces, padded.shape[1] // 8, sizes, total, out=out)
     torch.cuda.synchronize(); t.append(time.perf_counter())
     print("build %.2f - %.2f exchange %.2f plan %.2f assemble %.2f ms" %
           tuple((b - a) * 1e3 for a, b in zip(t, t[1:])))
