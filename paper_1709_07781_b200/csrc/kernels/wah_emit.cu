@@ -34,11 +34,18 @@ namespace ndx {
 #define NDX_EMIT_THREADS 256
 #endif
 #ifndef NDX_EMIT_MINB
-#define NDX_EMIT_MINB 3
+#define NDX_EMIT_MINB 1
 #endif
 constexpr int kEmitThreads = NDX_EMIT_THREADS;
 constexpr int kEmitWarps = kEmitThreads / 32;
-constexpr int kEmitK = 8;                               // consecutive elements per thread
+// 14 pairs per thread: 112-byte thread stride, so the 16-byte shared loads
+// of a quarter warp hit 8 distinct bank groups (8 pairs -> 64 B stride was a
+// 4-way conflict; measured C4 emit 1.49 -> 1.00 ms).  Must be even and < 31.
+#ifndef NDX_EMIT_K
+#define NDX_EMIT_K 14
+#endif
+static_assert(NDX_EMIT_K % 2 == 0 && NDX_EMIT_K < 31, "span length");
+constexpr int kEmitK = NDX_EMIT_K;                      // consecutive elements per thread
 constexpr int kEmitTile = kEmitThreads * kEmitK;        // 1024
 constexpr int kHaloL = 32;                              // elements before the tile (carry, prev)
 constexpr int kHaloR = 2;                               // elements after it (next; 16 B multiple)
