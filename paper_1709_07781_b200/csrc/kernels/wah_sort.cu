@@ -81,12 +81,26 @@ namespace ndx {
 #ifndef NDX_SORT_MATCH_TREE
 #define NDX_SORT_MATCH_TREE 0
 #endif
-template <int MAXB>
+// V = 1: the first byte pass (keys in, row ids synthesised) as its own
+// kernel -- with narrow keys its ranking needs no row registers, so it can
+// run more CTAs per SM than the later passes.
+#ifndef NDX_SORT_SPLIT_FIRST
+#define NDX_SORT_SPLIT_FIRST 0
+#endif
+#ifndef NDX_SORT_MINB_F
+#define NDX_SORT_MINB_F 3
+#endif
+#ifndef NDX_SORT_NARROW_F
+#define NDX_SORT_NARROW_F 1
+#endif
+template <int MAXB, int V = 0>
 struct Shape {
   static constexpr bool kWide = MAXB > 8;
+  static constexpr bool kFirst = V == 1;
   static constexpr int THREADS = kWide ? NDX_SORT_THREADS_W : NDX_SORT_THREADS_B;
   static constexpr int IPT = kWide ? NDX_SORT_IPT_W : NDX_SORT_IPT_B;  // pairs per thread
-  static constexpr int MINB = kWide ? NDX_SORT_MINB_W : NDX_SORT_MINB_B;
+  static constexpr int MINB = kWide ? NDX_SORT_MINB_W : (kFirst ? NDX_SORT_MINB_F : NDX_SORT_MINB_B);
+  static constexpr bool kNarrowOk = kWide ? NDX_SORT_NARROW_W : (kFirst ? NDX_SORT_NARROW_F : NDX_SORT_NARROW_B);
   static constexpr int WARPS = THREADS / 32;
   static constexpr int WARP_ITEMS = 32 * IPT;
   static constexpr int TILE = THREADS * IPT;
@@ -486,7 +500,11 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
 
   const uint32_t wofs = uint32_t(warp) * SH::WARP_ITEMS + lane;
   uint32_t key[SH::IPT], pay[SH::IPT];
-  if (t.in_pairs) {
+  // with the first byte pass split off, each kernel only ever sees one input
+  // form: the other load path is not compiled in
+  constexpr bool kOnlyKeys = SH::kFirst;
+  constexpr bool kOnlyPairs = !SH::kWide && !SH::kFirst && NDX_SORT_SPLIT_FIRST;
+  if (!kOnlyKeys && (kOnlyPairs || t.in_pairs)) {
     const uint64_t* pp = t.in_pairs + tile_start + wofs;
 #pragma unroll
     for (int r = 0; r < SH::IPT; ++r) {
@@ -697,7 +715,7 @@ __device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint3
     const uint64_t tile = *s_tile;
     if (tile >= tiles) return;
     const uint32_t tn = uint32_t(umin<uint64_t>(SH::TILE, n - tile * SH::TILE));
-    constexpr bool kNarrowOk = SH::kWide ? NDX_SORT_NARROW_W : NDX_SORT_NARROW_B;
+    constexpr bool kNarrowOk = SH::kNarrowOk;
     if (tn == uint32_t(SH::TILE)) {
       if (kNarrowOk && t.narrow)
         tile_pass<SH, BITS, NBMAX, true, true>(t, tile, tn);
@@ -714,12 +732,13 @@ __device__ __forceinline__ void tile_loop(const TileCtx& t, uint32_t* ctr, uint3
 
 // One stable scatter pass over persistent CTAs.  Pass q writes X iff
 // (P-1-q) is even, so the last pass lands in X.
-template <int MAXB>
-__global__ __launch_bounds__(Shape<MAXB>::THREADS, Shape<MAXB>::MINB) void k_pass(SortArgs a, int which) {
+template <int MAXB, int V = 0>
+__global__ __launch_bounds__(Shape<MAXB, V>::THREADS, Shape<MAXB, V>::MINB) void k_pass(SortArgs a, int which) {
   if (which < 0 && blockIdx.x == 0 && threadIdx.x == 0)
     a.ctl->row_hi = a.row_base + uint32_t(a.n - 1);  // read by the emit stage
   PassInfo pi;
   if (!pass_info(a, which, pi)) return;
+  if (MAXB == 8 && NDX_SORT_SPLIT_FIRST && ((pi.p == 0) != (V == 1))) return;  // the other kernel's pass
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = SortSmem<MAXB>;
   TileCtx t;
@@ -736,7 +755,7 @@ __global__ __launch_bounds__(Shape<MAXB>::THREADS, Shape<MAXB>::MINB) void k_pas
   t.epoch = pi.epoch;
   t.bstart = pi.bstart;
   t.status = a.status;
-  t.narrow = (MAXB > 8 ? NDX_SORT_NARROW_W : NDX_SORT_NARROW_B) && a.ctl->max_key < 65536u;
+  t.narrow = Shape<MAXB, V>::kNarrowOk && a.ctl->max_key < 65536u;
   t.H = reinterpret_cast<uint16_t*>(smem);
   t.S = reinterpret_cast<uint64_t*>(smem);
   t.cnt = reinterpret_cast<uint32_t*>(smem + SM::kUnion);
@@ -744,19 +763,19 @@ __global__ __launch_bounds__(Shape<MAXB>::THREADS, Shape<MAXB>::MINB) void k_pas
   uint32_t* s_tile = t.gbase + SM::NB;
   uint32_t* ctr = &a.ctl->tile_ctr[which + 2];  // [0] emit, [1] wide, [2..5] bytes
   if (MAXB == 8) {
-    tile_loop<Shape<MAXB>, 8, SM::NB>(t, ctr, s_tile, a.n);
+    tile_loop<Shape<MAXB, V>, 8, SM::NB>(t, ctr, s_tile, a.n);
   } else {
     // digits above `bits` are zero for every key, so a wider match is exact
     if (pi.bits <= 4)
-      tile_loop<Shape<MAXB>, 4, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB, V>, 4, SM::NB>(t, ctr, s_tile, a.n);
     else if (pi.bits <= 8)
-      tile_loop<Shape<MAXB>, 8, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB, V>, 8, SM::NB>(t, ctr, s_tile, a.n);
     else if (pi.bits <= 9)
-      tile_loop<Shape<MAXB>, 9, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB, V>, 9, SM::NB>(t, ctr, s_tile, a.n);
     else if (pi.bits <= 10)
-      tile_loop<Shape<MAXB>, 10, SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB, V>, 10, SM::NB>(t, ctr, s_tile, a.n);
     else
-      tile_loop<Shape<MAXB>, (MAXB > 10 ? 11 : 10), SM::NB>(t, ctr, s_tile, a.n);
+      tile_loop<Shape<MAXB, V>, (MAXB > 10 ? 11 : 10), SM::NB>(t, ctr, s_tile, a.n);
   }
 }
 
@@ -764,7 +783,7 @@ __global__ __launch_bounds__(Shape<MAXB>::THREADS, Shape<MAXB>::MINB) void k_pas
 
 struct LaunchCfg {
   int sms = 0;
-  int occ_wide = 1, occ_byte = 1;
+  int occ_wide = 1, occ_byte = 1, occ_first = 1;
   bool ready = false;
 };
 static LaunchCfg g_cfg[64];
@@ -789,6 +808,14 @@ static int launch_cfg(LaunchCfg** out) {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_pass<8>,
                                                            Shape<8>::THREADS, sb)))
       return e;
+#if NDX_SORT_SPLIT_FIRST
+    if ((e = cudaFuncSetAttribute(k_pass<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb))))
+      return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_first, k_pass<8, 1>,
+                                                           Shape<8, 1>::THREADS, sb)))
+      return e;
+    if (c.occ_first < 1) c.occ_first = 1;
+#endif
 #ifdef NDX_SORT_OCC_CAP
     c.occ_wide = umin(c.occ_wide, NDX_SORT_OCC_CAP);
     c.occ_byte = umin(c.occ_byte, NDX_SORT_OCC_CAP);
@@ -811,8 +838,13 @@ static int launch_sort(SortArgs a, cudaStream_t s, LaunchCfg* c) {
   const int gb = int(umin<uint64_t>(sort_tiles<8>(a.n), uint64_t(c->sms) * c->occ_byte));
   k_pass<kWideMaxBits>
       <<<gw, Shape<kWideMaxBits>::THREADS, SortSmem<kWideMaxBits>::kBytes, s>>>(a, -1);
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < 4; ++k) {
+#if NDX_SORT_SPLIT_FIRST
+    const int gf = int(umin<uint64_t>(sort_tiles<8>(a.n), uint64_t(c->sms) * c->occ_first));
+    k_pass<8, 1><<<gf, Shape<8, 1>::THREADS, SortSmem<8>::kBytes, s>>>(a, k);
+#endif
     k_pass<8><<<gb, Shape<8>::THREADS, SortSmem<8>::kBytes, s>>>(a, k);
+  }
   return cudaGetLastError();
 }
 
