@@ -198,3 +198,17 @@ def test_tile_boundaries(builder, port, n, kind):
     else:
         v = gen.zipf(n, n, 70000, 1.0)
     assert same(builder.build(v), port.reference_index(v)), (n, kind)
+
+
+@pytest.mark.parametrize("w", _digests().get("gpu_workloads", []), ids=lambda w: f"{w['kind']}-n{w['n']}-k{w['k']}")
+def test_largest_workload_digest(w):
+    """C5 (2^30 values, 65536 keys) on one GPU: the digest of the index equals
+    the oracle's, computed once on the GPU box (74 s of CPU) and stored."""
+    import oracle
+    from paper_1709_07781_b200 import ndx
+
+    v = gen.uniform(w["seed"], w["n"], w["k"])
+    b = ndx.WahBuilder(w["n"])
+    got = b.build(v)
+    assert got.words.size == w["W"] and len(got.entries) == w["D"]
+    assert "%016x" % oracle.Port().digest_parts(got.row_count, got.entries, got.words) == w["digest"]

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--ref", action="store_true", help="also the oracle's digest of the same values (slow)")
     a = ap.parse_args()
     v = gen.config_values(a.config, a.n or None)
     n = v.size
@@ -58,6 +59,11 @@ def main():
         got = b.fetch(n)
         d = oracle.Port().digest_parts(got.row_count, got.entries, got.words)
         print("  digest %016x" % d)
+        if a.ref:
+            import time as _t
+            t0 = _t.perf_counter()
+            r = oracle.Port().digest_of(v)
+            print("  oracle %016x (%s, %.0f s)" % (r, "match" if r == d else "MISMATCH", _t.perf_counter() - t0))
 
 
 if __name__ == "__main__":
