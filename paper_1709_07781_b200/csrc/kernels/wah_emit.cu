@@ -52,7 +52,10 @@ constexpr int kHaloR = 2;                               // elements after it (ne
 constexpr int kEmitBuf = kHaloL + kEmitTile + kHaloR;
 // staging of one tile: 2*kEmitTile words, then kEmitTile table-head values
 // and kEmitTile table-head word offsets (tile-local)
-constexpr int kStageTile = 4 * kEmitTile;
+// words (2 per pair at most), head values (u32) and head word offsets (u16:
+// below 2 * kEmitTile) -- u16 offsets keep two CTAs' worth of buffers in an SM
+constexpr int kStageTile = 3 * kEmitTile + kEmitTile / 2;
+static_assert(2 * kEmitTile < 65536, "head offsets are u16");
 constexpr size_t kEmitSmem = size_t(2 * kEmitBuf) * 8 + size_t(kStageTile) * 4;
 
 __device__ __forceinline__ uint32_t pkey(uint64_t e) { return uint32_t(e); }
@@ -218,7 +221,7 @@ __device__ __forceinline__ uint32_t bit_of(uint32_t pk, uint64_t e) {
 template <bool SMALL>
 __device__ __forceinline__ void span_emit(const Span& s, const uint64_t* Bs, uint32_t carry,
                                           uint32_t o, uint32_t h, uint32_t* stage, uint32_t* hv,
-                                          uint32_t* ho) {
+                                          uint16_t* ho) {
   // shared-space addresses, bumped per word: one STS per word, no generic
   // address arithmetic
   uint32_t sa = smem_addr(stage) + 4u * o;
@@ -245,7 +248,7 @@ __device__ __forceinline__ void span_emit(const Span& s, const uint64_t* Bs, uin
     const uint32_t gap = gap_of<SMALL>(s.pk[j]), bit = bit_of<SMALL>(s.pk[j], Bs[j]);
     if ((s.vmask >> j) & 1u) {
       hv[h] = pkey(Bs[j]);
-      ho[h] = (sa - sbase) >> 2;
+      ho[h] = uint16_t((sa - sbase) >> 2);
       ++h;
     }
     if (gap) {
@@ -484,7 +487,7 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[W0 + j] = stage[j];
       for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) {
         values[D0 + j] = stage[2 * kEmitTile + j];
-        vstart[D0 + j] = uint32_t(W0 + stage[3 * kEmitTile + j]);
+        vstart[D0 + j] = uint32_t(W0 + reinterpret_cast<const uint16_t*>(stage + 3 * kEmitTile)[j]);
       }
     }
     __syncthreads();  // the staging area is free again; s_tile[b^1] visible
@@ -496,9 +499,11 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       for (int w = 0; w < kEmitWarps; ++w) wbase += w < warp ? s_wt[b][w] : 0u;
       const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
       if (small_rows)
-        span_emit<true>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile, stage + 3 * kEmitTile);
+        span_emit<true>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile,
+                        reinterpret_cast<uint16_t*>(stage + 3 * kEmitTile));
       else
-        span_emit<false>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile, stage + 3 * kEmitTile);
+        span_emit<false>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile,
+                         reinterpret_cast<uint16_t*>(stage + 3 * kEmitTile));
     }
     pending = has ? int64_t(tile) : -1;
   }
