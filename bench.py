@@ -411,23 +411,33 @@ def run_ours(args, cfg):
     #      uploads its pinned keys, builds through the actor chain and writes
     #      counts + words + table back to pinned host memory.  Steps are
     #      pipelined two deep (ndactor_wah_build_index_async): step i+1's
-    #      upload overlaps step i's build and result copy (opposite PCIe
-    #      directions).  The fully synchronous call is timed once beside it.
+    #      upload and build overlap step i's result copy (opposite PCIe
+    #      directions, copy engines).  The fully synchronous call is timed
+    #      once beside it.
     hk = host_keys.numpy().view(np.uint32)
     ecap = 3 * max(65536, cfg["k"]) * 4
     hw = [torch.empty(2 * n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32) for _ in range(2)]
     he = [torch.empty(ecap, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32) for _ in range(2)]
     hc = [torch.zeros(3, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64) for _ in range(2)]
     e2e_steps = max(2, min(K, args.e2e_steps))
-    for i in range(2):  # warm both pipeline slots (first use allocates their key buffers)
-        rt.wait(rt.build_index_async(hk, hw[i], he[i], hc[i]))
+    # warm both pipeline slots with two builds in flight: the first use
+    # allocates the slots' key buffers and a second set of result buffers
+    warm = [rt.build_index_async(hk, hw[i], he[i], hc[i]) for i in range(2)]
+    for tk in warm:
+        rt.wait(tk)
     barrier()
     t0 = time.perf_counter()
     pend = []
+    trace = os.environ.get("NDX_E2E_TRACE")
     for i in range(e2e_steps):
+        ta = time.perf_counter()
         if len(pend) == 2:
             rt.wait(pend.pop(0))
+        tb = time.perf_counter()
         pend.append(rt.build_index_async(hk, hw[i % 2], he[i % 2], hc[i % 2]))
+        if trace:
+            print(f"e2e step {i}: wait {1e3 * (tb - ta):.1f} ms issue {1e3 * (time.perf_counter() - tb):.1f} ms",
+                  file=sys.stderr, flush=True)
     for tk in pend:
         rt.wait(tk)
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
@@ -486,7 +496,7 @@ def run_ours(args, cfg):
                      "traffic": traffic, "algorithmic_bytes": alg[dom]},
         "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": e2e_steps,
-                "pipelined": "2 deep: step i+1 upload overlaps step i build + result copy",
+                "pipelined": "2 deep: step i+1 upload (H2D) and build overlap step i result copy (D2H on the copy engines)",
                 "result_check_ok": e2e_ok, "sync_call_ms": e2e_sync_ms},
         "gpu_launches": 11 * K,
         "clocks": clk,
@@ -513,7 +523,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
     ap.add_argument("--n", type=int, default=0, help="values per GPU (default: the config's)")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3 line inside the C4 report")

@@ -43,11 +43,13 @@ int ndactor_wah_build_index(ndactor_runtime* rt, const uint32_t* values, uint64_
                             uint64_t* n_words, uint64_t* n_entries);
 
 /* Pipelined variant of ndactor_wah_build_index for a stream of columns:
- * returns at once.  The upload of `values` (pinned host memory) runs on its
- * own stream, so it overlaps the previous build and the previous result's
- * copy to the host; the result (counts, then up to words_cap words and
- * entries_cap table words, all pinned host memory) is written by the GPU
- * with no host round trip for the sizes.  At most two builds in flight:
+ * returns at once.  Three streams keep both PCIe directions and the SMs busy:
+ * the upload of `values` (pinned host memory) on its own stream, the build
+ * on the device stream, and the result copy on an egress stream.  The build
+ * ends with a copy of the counts to pinned memory; an egress thread then
+ * issues exactly min(W, words_cap) words and min(3D, entries_cap) table
+ * words of device-to-host copy (copy engines, no SMs).  So step i's result
+ * copy overlaps step i+1's upload and build.  At most two builds in flight:
  * call ndactor_wah_wait(ticket) before reusing a ticket's buffers.  The
  * inputs must stay untouched until then.  counts->words / ->distinct give
  * the true sizes even if the capacities were too small. */

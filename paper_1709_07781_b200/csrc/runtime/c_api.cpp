@@ -2,9 +2,13 @@
 #include "ndactor_c.h"
 
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <future>
+#include <mutex>
 #include <string>
+#include <thread>
 
 #include "ndactor/compute_actor.hpp"
 #include "ndactor/wah_device.hpp"
@@ -22,25 +26,96 @@ struct ndactor_runtime {
   std::uint32_t shard_base = 0;
   wah::DeviceIndex last;   // result of the last device build (kept alive)
   ActorHandle probe;
-  // pipelined host builds: uploads run on their own stream (the other copy
-  // direction of the PCIe link) while the previous build and its result
-  // copy run on the device stream
+  // Pipelined host builds.  Three streams, so both PCIe directions and the
+  // SMs work at once: uploads on `upload`, the build on the device stream,
+  // the result copy on `egress` (the copy engines, no SMs).  The result size
+  // is known only on the device: the build's last command copies the counts
+  // to pinned memory and hands the slot to the egress thread, which issues
+  // exactly W + 3D words of D2H once the counts have landed.
   struct Slot {
     Buffer keys;
     std::uint64_t cap = 0;
     void* uploaded = nullptr;  // cudaEvent: keys are on the device
+    void* built = nullptr;     // cudaEvent: the counts are in `hc`
     void* done = nullptr;      // cudaEvent: the result is in host memory
+    ndx_wah_counts* hc = nullptr;  // pinned
+    MemRef cfg, words, entries;    // device result, held until the copy is done
+    uint32_t* h_words = nullptr;
+    uint32_t* h_entries = nullptr;
+    std::uint64_t words_cap = 0, entries_cap = 0;
+    ndx_wah_counts* counts = nullptr;
     bool busy = false;
+    bool issued = false;  // egress has issued the copy (or failed)
+    int rc = 0;
   };
   void* upload = nullptr;
+  void* egress = nullptr;
   Slot slots[2];
   std::uint64_t next_ticket = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<int> jobs;
+  bool stop = false;
+  std::thread egress_thread;
+
+  void egress_loop() {
+    for (;;) {
+      int j;
+      {
+        std::unique_lock<std::mutex> l(mu);
+        cv.wait(l, [&] { return stop || !jobs.empty(); });
+        if (jobs.empty()) return;
+        j = jobs.front();
+        jobs.pop_front();
+      }
+      Slot& sl = slots[j];
+      int rc = ndx_event_synchronize(sl.built);
+      if (!rc) {
+        const ndx_wah_counts c = *sl.hc;
+        *sl.counts = c;
+        const std::uint64_t nw = std::min<std::uint64_t>(c.words, sl.words_cap);
+        const std::uint64_t ne = std::min<std::uint64_t>(3 * c.distinct, sl.entries_cap);
+        if (nw) rc = ndx_memcpy_d2h_async(sl.h_words, sl.words.buffer().data(), nw * 4, egress);
+        if (!rc && ne) rc = ndx_memcpy_d2h_async(sl.h_entries, sl.entries.buffer().data(), ne * 4, egress);
+        if (!rc) rc = ndx_event_record(sl.done, egress);
+      }
+      {
+        std::lock_guard<std::mutex> l(mu);
+        sl.issued = true;
+        sl.rc = rc;
+      }
+      cv.notify_all();
+    }
+  }
+  void post(int j, int rc) {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      if (rc) {
+        slots[j].issued = true;
+        slots[j].rc = rc;
+      } else {
+        jobs.push_back(j);
+      }
+    }
+    cv.notify_all();
+  }
   ~ndactor_runtime() {
+    if (egress_thread.joinable()) {
+      {
+        std::lock_guard<std::mutex> l(mu);
+        stop = true;
+      }
+      cv.notify_all();
+      egress_thread.join();
+    }
     for (Slot& s : slots) {
       if (s.uploaded) ndx_event_destroy(s.uploaded);
+      if (s.built) ndx_event_destroy(s.built);
       if (s.done) ndx_event_destroy(s.done);
+      if (s.hc) ndx_host_free(s.hc);
     }
     if (upload) ndx_stream_destroy(upload);
+    if (egress) ndx_stream_destroy(egress);
   }
 };
 
@@ -148,16 +223,22 @@ int ndactor_wah_build_index_async(ndactor_runtime* rt, const uint32_t* values, u
   return guarded([&] {
     if (!rt || !counts || !ticket) throw std::invalid_argument("null argument");
     if (n == 0) throw std::invalid_argument("empty input");
+    if ((!words && words_cap) || (!entries && entries_cap)) throw std::invalid_argument("null output buffer");
     Device& dev = *rt->dev;
     auto ck = [](int rc, const char* what) {
       if (rc) throw std::runtime_error(std::string(what) + ": " + ndx_error_string(rc));
     };
     if (!rt->upload) ck(ndx_stream_create(&rt->upload), "upload stream");
+    if (!rt->egress) ck(ndx_stream_create(&rt->egress), "egress stream");
+    if (!rt->egress_thread.joinable()) rt->egress_thread = std::thread([rt] { rt->egress_loop(); });
     const std::uint64_t t = rt->next_ticket;
-    ndactor_runtime::Slot& sl = rt->slots[t & 1];
+    const int j = int(t & 1);
+    ndactor_runtime::Slot& sl = rt->slots[j];
     if (sl.busy) throw std::runtime_error("two builds already in flight: wait for one first");
     if (!sl.uploaded) ck(ndx_event_create(&sl.uploaded, 0), "event");
+    if (!sl.built) ck(ndx_event_create(&sl.built, 0), "event");
     if (!sl.done) ck(ndx_event_create(&sl.done, 0), "event");
+    if (!sl.hc) ck(ndx_host_alloc(reinterpret_cast<void**>(&sl.hc), sizeof(ndx_wah_counts)), "pinned counts");
     if (sl.cap < n) {
       if (sl.keys.valid()) {
         dev.await_all();
@@ -167,7 +248,8 @@ int ndactor_wah_build_index_async(ndactor_runtime* rt, const uint32_t* values, u
       sl.cap = n;
       dev.await_all();
     }
-    // the slot's keys were last read by build t-2: its `done` orders the upload
+    // the slot's keys were last read by build t-2, whose result copy (`done`)
+    // came after it
     ck(ndx_stream_wait_event(rt->upload, sl.done), "upload wait");
     ck(ndx_memcpy_h2d_async(sl.keys.data(), values, n * 4, rt->upload), "upload");
     ck(ndx_event_record(sl.uploaded, rt->upload), "upload record");
@@ -176,22 +258,33 @@ int ndactor_wah_build_index_async(ndactor_runtime* rt, const uint32_t* values, u
     // the chain releases its input MemRef: hand it a non-owning view of the slot
     Buffer view = dev.wrap_buffer(sl.keys.data(), ElemType::u32, std::int64_t(n), Access::read_only);
     wah::DeviceIndex d = wah::build_index_device(*rt->sys, rt->stages, MemRef(view, ready), std::uint32_t(n));
-    void* done = sl.done;
+    sl.cfg = d.cfg;
+    sl.words = d.words;
+    sl.entries = d.entries;
+    sl.h_words = words;
+    sl.h_entries = entries;
+    sl.words_cap = words_cap;
+    sl.entries_cap = entries_cap;
+    sl.counts = counts;
+    sl.issued = false;
+    sl.rc = 0;
     std::vector<Event> deps{d.entries.pending(), d.words.pending(), d.cfg.pending()};
     const void* cfg = d.cfg.buffer().data();
-    const uint32_t* dw = static_cast<const uint32_t*>(d.words.buffer().data());
-    const uint32_t* de = static_cast<const uint32_t*>(d.entries.buffer().data());
-    dev.enqueue_native(
-        "copy_out",
+    ndx_wah_counts* hc = sl.hc;
+    void* built = sl.built;
+    Event counted = dev.enqueue_native(
+        "counts_d2h",
         [=](void* s) -> int {
-          int rc = ndx_wah_copy_out(cfg, dw, de, counts, words, words_cap, entries, entries_cap, s);
-          if (!rc) rc = ndx_event_record(done, s);
+          int rc = ndx_memcpy_d2h_async(hc, cfg, sizeof(ndx_wah_counts), s);
+          if (!rc) rc = ndx_event_record(built, s);
+          rt->post(j, rc);
           return rc;
         },
         deps);
-    release(d.cfg);
-    release(d.words);
-    release(d.entries);
+    // a command that never runs (device failure upstream) still ends the wait
+    counted.add_callback([rt, j](EventState st) {
+      if (st == EventState::failed) rt->post(j, -1);
+    });
     sl.busy = true;
     rt->next_ticket = t + 1;
     *ticket = t;
@@ -204,10 +297,20 @@ int ndactor_wah_wait(ndactor_runtime* rt, uint64_t ticket) {
     if (!rt) throw std::invalid_argument("null runtime");
     ndactor_runtime::Slot& sl = rt->slots[ticket & 1];
     if (!sl.busy) return 0;
-    (void)rt->dev->stream();  // every queued launch issued before waiting on the event
-    const int rc = ndx_event_synchronize(sl.done);
+    (void)rt->dev->stream();  // every queued launch issued
+    int rc;
+    {
+      std::unique_lock<std::mutex> l(rt->mu);
+      rt->cv.wait(l, [&] { return sl.issued; });
+      rc = sl.rc;
+    }
+    if (!rc) rc = ndx_event_synchronize(sl.done);
+    release(sl.cfg);
+    release(sl.words);
+    release(sl.entries);
+    sl.cfg = sl.words = sl.entries = MemRef{};
     sl.busy = false;
-    if (rc) throw std::runtime_error(std::string("build failed: ") + ndx_error_string(rc));
+    if (rc) throw std::runtime_error(std::string("build failed: ") + (rc > 0 ? ndx_error_string(rc) : "device failure"));
     return 0;
   });
 }

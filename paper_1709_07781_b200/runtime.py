@@ -106,9 +106,11 @@ class Runtime:
 
     def build_index_async(self, values: np.ndarray, words_out: np.ndarray, entries_out: np.ndarray,
                           counts_out: np.ndarray) -> int:
-        """Pipelined build (ndactor_wah_build_index_async): all four arrays
-        must be pinned host memory and stay untouched until wait(ticket).
-        counts_out: 3 x u64 (words, distinct, min | max << 32)."""
+        """Pipelined build (ndactor_wah_build_index_async): the arrays must
+        stay untouched until wait(ticket); pinned host memory keeps the
+        copies at full PCIe speed.  Output sizes are the capacities (a
+        result longer than them is cut, counts_out still holds the true
+        sizes).  counts_out: 3 x u64 (words, distinct, min | max << 32)."""
         v = values
         t = _u64()
         _check(self.lib.ndactor_wah_build_index_async(

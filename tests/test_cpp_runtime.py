@@ -59,8 +59,8 @@ def test_runtime_dispatch_probe_counts_every_kernel():
 
 @pytest.mark.gpu
 def test_runtime_async_pipeline_matches_oracle(port):
-    """ndactor_wah_build_index_async: two builds in flight, results written
-    by the GPU straight into pinned host memory, bit-exact."""
+    """ndactor_wah_build_index_async: two builds in flight, results copied
+    to pinned host memory on the egress stream, bit-exact."""
     import torch
 
     from paper_1709_07781_b200 import gen
@@ -88,4 +88,30 @@ def test_runtime_async_pipeline_matches_oracle(port):
         W, D = int(c[0]), int(c[1])
         assert W == ref.words.size and D == len(ref.entries)
         assert np.array_equal(w[:W], ref.words) and np.array_equal(e[:3 * D].reshape(-1, 3), ref.entries)
+    rt.close()
+
+
+@pytest.mark.gpu
+def test_runtime_async_small_capacity_and_pageable(port):
+    """Capacities below the result: the true counts come back and exactly
+    the prefix that fits is written (nothing past it); pageable output
+    memory works too."""
+    from paper_1709_07781_b200 import gen
+    from paper_1709_07781_b200.runtime import Runtime
+
+    rt = Runtime()
+    v = gen.zipf(9, 200_000, 2000, 1.0)
+    ref = port.reference_index(v)
+    W, D = ref.words.size, len(ref.entries)
+    w = np.full(W // 3 + 2, 0xDEADBEEF, np.uint32)
+    e = np.full(3 * (D // 2) + 3, 0xDEADBEEF, np.uint32)
+    c = np.zeros(3, np.uint64)
+    rt.wait(rt.build_index_async(v, w[:-2], e[:-3], c))
+    assert int(c[0]) == W and int(c[1]) == D
+    assert np.array_equal(w[:-2], ref.words[:w.size - 2]) and (w[-2:] == 0xDEADBEEF).all()
+    assert np.array_equal(e[:-3], ref.entries.reshape(-1)[:e.size - 3]) and (e[-3:] == 0xDEADBEEF).all()
+    # zero capacities: counts only
+    c2 = np.zeros(3, np.uint64)
+    rt.wait(rt.build_index_async(v, w[:0], e[:0], c2))
+    assert int(c2[0]) == W and int(c2[1]) == D
     rt.close()
