@@ -78,6 +78,10 @@ namespace ndx {
 #ifndef NDX_SORT_ATOMRANK
 #define NDX_SORT_ATOMRANK 0
 #endif
+// wide keys: two ranks (< 2^16) per register, 16 fewer live registers
+#ifndef NDX_SORT_PACK_RANK
+#define NDX_SORT_PACK_RANK 1
+#endif
 #ifndef NDX_SORT_MATCH_TREE
 #define NDX_SORT_MATCH_TREE 0
 #endif
@@ -542,7 +546,17 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
 #endif
 
   // ---- rank
-  uint32_t rank[NARROW ? 1 : SH::IPT];
+  static_assert(SH::TILE <= 65536 && SH::IPT % 2 == 0, "packed ranks need 16-bit tile slots");
+  constexpr bool PACK = NDX_SORT_PACK_RANK && !NARROW;
+  uint32_t rank[NARROW ? 1 : (PACK ? SH::IPT / 2 : SH::IPT)] = {};
+  // rank of round r: in rank[r] or, packed, in half (r & 1) of rank[r / 2]
+  auto rank_add = [&](int r, uint32_t v) {
+    if (PACK)
+      rank[r >> 1] += v << (16 * (r & 1));
+    else
+      rank[r] += v;
+  };
+  auto rank_get = [&](int r) -> uint32_t { return PACK ? (rank[r >> 1] >> (16 * (r & 1))) & 0xffffu : rank[r]; };
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r) {
     const uint32_t d = digit(key[r]);
@@ -576,6 +590,10 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
 #endif
     if (NARROW)
       key[r] |= rk << 16;
+    else if (PACK && (r & 1) == 0)
+      rank[r >> 1] = rk;
+    else if (PACK)
+      rank[r >> 1] |= rk << 16;
     else
       rank[r] = rk;
   }
@@ -624,7 +642,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     if (NARROW)
       key[r] += uint32_t(Hw[d]) << 16;
     else
-      rank[r] += Hw[d];
+      rank_add(r, Hw[d]);
   }
   __syncthreads();  // H no longer read: S may overwrite it
 #pragma unroll
@@ -633,7 +651,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       if (NARROW)
         t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay[r]) << 32);
       else
-        t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+        t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
     }
   // ---- look-back, part 2: finish from the status already in hand
 #pragma unroll
@@ -671,7 +689,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     if (NARROW)
       key[r] += uint32_t(Hw[d]) << 16;
     else
-      rank[r] += Hw[d];
+      rank_add(r, Hw[d]);
   }
   __syncthreads();  // H no longer read: S may overwrite it
 #pragma unroll
@@ -680,7 +698,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       if (NARROW)
         t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay[r]) << 32);
       else
-        t.S[rank[r]] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+        t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
     }
   __syncthreads();
   }
