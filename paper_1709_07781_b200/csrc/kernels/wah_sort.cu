@@ -119,7 +119,13 @@ constexpr int kHistThreads = 512;
 // key, not 3), and every group of four warps counts into its own copy so a
 // skewed column's hot bins are not one shared-memory hot spot.
 constexpr int kHistCopies = 4;
-__global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restrict__ keys,
+#ifndef NDX_HIST_PIPE
+#define NDX_HIST_PIPE 1
+#endif
+#ifndef NDX_HIST_MINB
+#define NDX_HIST_MINB 1
+#endif
+__global__ __launch_bounds__(kHistThreads, NDX_HIST_MINB) void k_hist(const uint32_t* __restrict__ keys,
                                                        uint64_t n, Ctl* ctl) {
   __shared__ uint32_t hws[kHistCopies][kWideBuckets], h1s[kHistCopies][256];
   for (int i = threadIdx.x; i < kHistCopies * kWideBuckets; i += blockDim.x) (&hws[0][0])[i] = 0;
@@ -141,6 +147,31 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restric
     const uint4* q = reinterpret_cast<const uint4*>(keys);
     const uint64_t nq = n / 4;
     uint64_t i = tid;
+#if NDX_HIST_PIPE
+    // 4 loads in flight, and the next 4 issued before this batch's atomics
+    if (i + 3 * stride < nq) {
+      uint4 v0 = ldg_stream4(q + i), v1 = ldg_stream4(q + i + stride);
+      uint4 v2 = ldg_stream4(q + i + 2 * stride), v3 = ldg_stream4(q + i + 3 * stride);
+      for (;;) {
+        const uint64_t nx = i + 4 * stride;
+        const bool more = nx + 3 * stride < nq;
+        uint4 w0 = v0, w1 = v1, w2 = v2, w3 = v3;
+        if (more) {
+          w0 = ldg_stream4(q + nx);
+          w1 = ldg_stream4(q + nx + stride);
+          w2 = ldg_stream4(q + nx + 2 * stride);
+          w3 = ldg_stream4(q + nx + 3 * stride);
+        }
+        one(v0.x); one(v0.y); one(v0.z); one(v0.w);
+        one(v1.x); one(v1.y); one(v1.z); one(v1.w);
+        one(v2.x); one(v2.y); one(v2.z); one(v2.w);
+        one(v3.x); one(v3.y); one(v3.z); one(v3.w);
+        i = nx;
+        if (!more) break;
+        v0 = w0; v1 = w1; v2 = w2; v3 = w3;
+      }
+    }
+#else
     for (; i + 3 * stride < nq; i += 4 * stride) {  // 4 loads in flight
       const uint4 v0 = ldg_stream4(q + i), v1 = ldg_stream4(q + i + stride);
       const uint4 v2 = ldg_stream4(q + i + 2 * stride), v3 = ldg_stream4(q + i + 3 * stride);
@@ -149,6 +180,7 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const uint32_t* __restric
       one(v2.x); one(v2.y); one(v2.z); one(v2.w);
       one(v3.x); one(v3.y); one(v3.z); one(v3.w);
     }
+#endif
     for (; i < nq; i += stride) {
       const uint4 v = ldg_stream4(q + i);
       one(v.x); one(v.y); one(v.z); one(v.w);
@@ -870,7 +902,11 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, uint32_t* epo
                        cudaStream_t s, LaunchCfg* c) {
   cudaError_t e = cudaMemsetAsync(ctl, 0, offsetof(Ctl, zero_end), s);
   if (e) return e;
-  const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * 4, (n + 65535) / 65536)));
+  // one wave: every CTA resident (a second partial wave would run alone)
+  static int hist_occ = 0;
+  if (!hist_occ && (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hist_occ, k_hist, kHistThreads, 0)))
+    return e;
+  const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * umax(hist_occ, 1), (n + 65535) / 65536)));
   k_hist<<<grid, kHistThreads, 0, s>>>(keys, n, ctl);
   k_plan<<<1, 1024, 0, s>>>(ctl, n, 0, epoch_counter);
   k_hist_hi<<<c->sms * 2, kHistThreads, 0, s>>>(keys, n, ctl);
