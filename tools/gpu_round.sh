@@ -8,6 +8,7 @@ O=gpurun_out/$TAG
 mkdir -p $O
 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 tail -3 $O/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> $O/${TAG}_smoke.log
 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 cat $O/bench.json
 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2>>$O/bench.err
