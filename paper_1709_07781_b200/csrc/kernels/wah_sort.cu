@@ -88,6 +88,9 @@ namespace ndx {
 // V = 1: the first byte pass (keys in, row ids synthesised) as its own
 // kernel -- with narrow keys its ranking needs no row registers, so it can
 // run more CTAs per SM than the later passes.
+#ifndef NDX_SORT_PROF
+#define NDX_SORT_PROF 0
+#endif
 #ifndef NDX_SORT_SPLIT_FIRST
 #define NDX_SORT_SPLIT_FIRST 0
 #endif
@@ -521,8 +524,30 @@ __device__ __forceinline__ uint64_t lookback_from(const uint64_t* st, uint64_t t
 // NARROW: every key is below 2^16 (known from the plan), so a pair's rank
 // rides in the upper half of its key register -- 32 fewer live registers in
 // the ranking, no spills.
+#if NDX_SORT_PROF
+// experiment build only: cycles per tile phase, summed over tiles by thread 0
+// of each CTA (load, rank, counts+scan, look-back+staging, scatter)
+__device__ unsigned long long g_sort_prof[8];
+#define PROF_MARK(i)                                                     \
+  do {                                                                   \
+    if (threadIdx.x == 0) {                                              \
+      const long long now_ = clock64();                                  \
+      atomicAdd(&g_sort_prof[i], (unsigned long long)(now_ - prof_t_));  \
+      prof_t_ = now_;                                                    \
+    }                                                                    \
+  } while (0)
+#else
+#define PROF_MARK(i) \
+  do {               \
+  } while (0)
+#endif
+
 template <class SH, int BITS, int NBMAX, bool FULL, bool NARROW>
 __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint32_t tile_n) {
+#if NDX_SORT_PROF
+  long long prof_t_ = clock64();
+  if (threadIdx.x == 0) atomicAdd(&g_sort_prof[7], 1ull);
+#endif
   constexpr uint32_t NB = 1u << BITS;
   constexpr uint32_t DMASK = NB - 1;
   auto digit = [&](uint32_t k) -> uint32_t {
@@ -535,12 +560,13 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) t.cnt[d] = 0;
 
   const uint32_t wofs = uint32_t(warp) * SH::WARP_ITEMS + lane;
-  uint32_t key[SH::IPT], pay[SH::IPT];
-  // with the first byte pass split off, each kernel only ever sees one input
-  // form: the other load path is not compiled in
+  // kFirst (the split-off first byte pass): keys in, row ids synthesised at
+  // staging time -- no row registers at all
   constexpr bool kOnlyKeys = SH::kFirst;
-  constexpr bool kOnlyPairs = !SH::kWide && !SH::kFirst && NDX_SORT_SPLIT_FIRST;
-  if (!kOnlyKeys && (kOnlyPairs || t.in_pairs)) {
+  uint32_t key[SH::IPT], pay[kOnlyKeys ? 1 : SH::IPT];
+  const uint32_t r0 = t.row_base + uint32_t(tile_start) + wofs;
+  auto pay_at = [&](int r) -> uint32_t { return kOnlyKeys ? r0 + uint32_t(r) * 32u : pay[r]; };
+  if (!kOnlyKeys && t.in_pairs) {
     const uint64_t* pp = t.in_pairs + tile_start + wofs;
 #pragma unroll
     for (int r = 0; r < SH::IPT; ++r) {
@@ -553,18 +579,20 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
 #pragma unroll
     for (int r = 0; r < SH::IPT; ++r)
       key[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(kp + r * 32) : 0u;
-    if (t.in_pays) {
-      const uint32_t* rp = t.in_pays + tile_start + wofs;
+    if (!kOnlyKeys) {
+      if (t.in_pays) {
+        const uint32_t* rp = t.in_pays + tile_start + wofs;
 #pragma unroll
-      for (int r = 0; r < SH::IPT; ++r)
-        pay[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(rp + r * 32) : 0u;
-    } else {
-      const uint32_t r0 = t.row_base + uint32_t(tile_start) + wofs;
+        for (int r = 0; r < SH::IPT; ++r)
+          pay[r] = (FULL || wofs + r * 32 < tile_n) ? ldg_stream(rp + r * 32) : 0u;
+      } else {
 #pragma unroll
-      for (int r = 0; r < SH::IPT; ++r) pay[r] = r0 + r * 32;
+        for (int r = 0; r < SH::IPT; ++r) pay[r] = r0 + r * 32;
+      }
     }
   }
   __syncthreads();
+  PROF_MARK(0);
 
   uint64_t* st = t.status + tile * NB;
 #if !NDX_SORT_LATE_COUNT
@@ -630,6 +658,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       rank[r] = rk;
   }
   __syncthreads();
+  PROF_MARK(1);
 
   // ---- per digit: warp offsets (in place); tile-local digit starts
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
@@ -650,6 +679,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   __syncthreads();  // the scan reads other threads' counts
 #endif
   block_excl_scan(t.cnt, t.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+  PROF_MARK(2);
 
   if constexpr (SH::kWide ? NDX_SORT_EARLY_LB_W : NDX_SORT_EARLY_LB_B) {
   // ---- look-back, part 1: the first predecessor status of each of this
@@ -681,9 +711,9 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   for (int r = 0; r < SH::IPT; ++r)
     if (FULL || wofs + r * 32 < tile_n) {
       if (NARROW)
-        t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay[r]) << 32);
+        t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay_at(r)) << 32);
       else
-        t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+        t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay_at(r)) << 32);
     }
   // ---- look-back, part 2: finish from the status already in hand
 #pragma unroll
@@ -699,6 +729,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     t.gbase[d] = t.bstart[d] + uint32_t(excl) - local;
   }
   __syncthreads();
+  PROF_MARK(3);
   } else {
   // ---- look-back: global base of each digit for this tile
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
@@ -728,9 +759,9 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
   for (int r = 0; r < SH::IPT; ++r)
     if (FULL || wofs + r * 32 < tile_n) {
       if (NARROW)
-        t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay[r]) << 32);
+        t.S[key[r] >> 16] = uint64_t(key[r] & 0xffffu) | (uint64_t(pay_at(r)) << 32);
       else
-        t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay[r]) << 32);
+        t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay_at(r)) << 32);
     }
   __syncthreads();
   }
@@ -753,6 +784,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     }
   }
   __syncthreads();
+  PROF_MARK(4);
 }
 
 template <class SH, int BITS, int NBMAX>
@@ -788,7 +820,10 @@ __global__ __launch_bounds__(Shape<MAXB, V>::THREADS, Shape<MAXB, V>::MINB) void
     a.ctl->row_hi = a.row_base + uint32_t(a.n - 1);  // read by the emit stage
   PassInfo pi;
   if (!pass_info(a, which, pi)) return;
-  if (MAXB == 8 && NDX_SORT_SPLIT_FIRST && ((pi.p == 0) != (V == 1))) return;  // the other kernel's pass
+  // the split-off first pass takes pass 0 of a row-id sort (no payload input)
+  const bool split0 = NDX_SORT_SPLIT_FIRST && a.in_payloads == nullptr;
+  if (V == 1 && !(split0 && pi.p == 0)) return;
+  if (MAXB == 8 && V == 0 && split0 && pi.p == 0) return;  // the other kernel's pass
   extern __shared__ __align__(16) unsigned char smem[];
   using SM = SortSmem<MAXB>;
   TileCtx t;
@@ -1004,3 +1039,14 @@ int ndx_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_payloads, uint64_t n, void*
 }
 
 }  // extern "C"
+
+#if NDX_SORT_PROF
+extern "C" int ndx_sort_prof_read(unsigned long long* h, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(h, ndx::g_sort_prof, sizeof(ndx::g_sort_prof));
+  if (!e && reset) {
+    unsigned long long z[8] = {};
+    e = cudaMemcpyToSymbol(ndx::g_sort_prof, z, sizeof(z));
+  }
+  return e;
+}
+#endif

@@ -108,6 +108,7 @@ struct ndactor_runtime {
       cv.notify_all();
       egress_thread.join();
     }
+    if (egress) ndx_stream_synchronize(egress);  // copies issued but never waited for
     for (Slot& s : slots) {
       if (s.uploaded) ndx_event_destroy(s.uploaded);
       if (s.built) ndx_event_destroy(s.built);

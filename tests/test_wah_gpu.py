@@ -4,6 +4,7 @@ oracle and the reference-generated golden fixtures.  Bit-exact, no tolerance.
 Mirrors p/tests/test_wah_device.cpp:45-274 and acceptance.cpp checks 1-3."""
 import json
 import os
+import zlib
 
 import numpy as np
 import pytest
@@ -57,9 +58,10 @@ def test_single_row_and_empty(builder, port):  # test_wah_device.cpp:232-244
 
 
 @pytest.mark.parametrize("case", ["long_stretch", "stretch_tile_edges", "sorted_blocks", "mode_edges",
-                                  "full_range", "hi_bytes", "constant", "two_values_alt"])
+                                  "full_range", "hi_bytes", "constant", "two_values_alt", "wide_high_base",
+                                  "bytes_0_and_2", "wide_high_base_big"])
 def test_adversarial_shapes(builder, port, case):
-    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
     if case == "long_stretch":  # ones-stretches spanning many emit tiles
         v = np.repeat(np.array([3, 1, 4, 1, 5], np.uint32), [200_000, 31 * 5000, 93, 31 * 777 + 5, 10])
     elif case == "stretch_tile_edges":
@@ -77,6 +79,12 @@ def test_adversarial_shapes(builder, port, case):
         v[100] = 0x80000000
     elif case == "hi_bytes":  # bytes 2/3 vary, 0/1 constant
         v = (rng.integers(0, 300, 100_000).astype(np.uint32) << 16) | 0x1234
+    elif case == "wide_high_base":  # one wide pass, keys above 2^16 (no narrow packing)
+        v = (3_000_000_000 + rng.integers(0, 2000, 150_000)).astype(np.uint32)
+    elif case == "wide_high_base_big":  # the same over many full 16384-pair tiles
+        v = (0xFFFFF000 + rng.zipf(1.3, 1_500_000) % 2040).astype(np.uint32)
+    elif case == "bytes_0_and_2":  # two byte passes with a constant byte between them
+        v = (rng.integers(0, 256, 120_000).astype(np.uint32) << 16) | rng.integers(0, 256, 120_000).astype(np.uint32) | 0x4200
     elif case == "constant":
         v = np.full(123_457, 0xFFFFFFFF, np.uint32)
     else:
