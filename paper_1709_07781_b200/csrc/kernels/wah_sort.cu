@@ -526,7 +526,7 @@ __device__ __forceinline__ uint64_t lookback_from(const uint64_t* st, uint64_t t
 // the ranking, no spills.
 #if NDX_SORT_PROF
 // experiment build only: cycles per tile phase, summed over tiles by thread 0
-// of each CTA (load, rank, counts+scan, look-back+staging, scatter)
+// of each CTA (load, rank, counts+scan, staging, look-back, scatter)
 __device__ unsigned long long g_sort_prof[8];
 #define PROF_MARK(i)                                                     \
   do {                                                                   \
@@ -715,6 +715,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
       else
         t.S[rank_get(r)] = uint64_t(key[r]) | (uint64_t(pay_at(r)) << 32);
     }
+  PROF_MARK(3);
   // ---- look-back, part 2: finish from the status already in hand
 #pragma unroll
   for (int k = 0; k < ND; ++k) {
@@ -729,7 +730,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     t.gbase[d] = t.bstart[d] + uint32_t(excl) - local;
   }
   __syncthreads();
-  PROF_MARK(3);
+  PROF_MARK(4);
   } else {
   // ---- look-back: global base of each digit for this tile
   for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
@@ -784,7 +785,7 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     }
   }
   __syncthreads();
-  PROF_MARK(4);
+  PROF_MARK(5);
 }
 
 template <class SH, int BITS, int NBMAX>

@@ -3,7 +3,7 @@
     python tools/variants.py prof=-DNDX_SORT_PROF=1
     NDX_LIB=libndx_prof.so python tools/sort_prof.py C4
 Prints, per tile and CTA, the mean cycles of: load, rank, counts+scan,
-look-back+staging, scatter (thread 0's clock between the block barriers)."""
+staging, look-back, scatter (thread 0's clock between the block barriers)."""
 import ctypes
 import os
 import sys
@@ -34,8 +34,8 @@ def main():
             fn(buf, 1)
     fn(buf, 0)
     tiles = buf[7]
-    names = ["load", "rank", "counts+scan", "lookback+stage", "scatter"]
-    tot = sum(buf[i] for i in range(5))
+    names = ["load", "rank", "counts+scan", "stage", "lookback", "scatter"]
+    tot = sum(buf[i] for i in range(6))
     print(f"{cfg}: {tiles} tiles over 3 builds")
     for i, nm in enumerate(names):
         print(f"  {nm:15s} {buf[i] / tiles:9.0f} cycles/tile  {100 * buf[i] / tot:5.1f}%")
