@@ -307,6 +307,7 @@ def extra_config(rt, raw, dev, K, W_, name="C3"):
     a0.record(rts)
     for _ in range(K):
         rt.build_index_device(keys.data_ptr(), n)
+    rt.synchronize()  # every stage issued (actor hops, launcher ring) and done
     a1.record(rts)
     a1.synchronize()
     ms = a0.elapsed_time(a1) / K
@@ -386,6 +387,10 @@ def run_ours(args, cfg):
     a0.record(rts)
     for _ in range(K):
         rt.build_index_device(keys.data_ptr(), n)
+    # the requests return once queued: the stages reach the stream through
+    # the actor hops and the launcher thread, so the end event is recorded
+    # only after everything was issued and has finished
+    rt.synchronize()
     a1.record(rts)
     barrier()
     a1.synchronize()
