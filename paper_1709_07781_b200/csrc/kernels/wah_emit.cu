@@ -294,6 +294,7 @@ __device__ __forceinline__ uint32_t warp_carry(const uint64_t* B, uint32_t ts, u
 // Tiles whose halo lies inside [0, n) arrive by one bulk async copy (TMA,
 // mbarrier completion) issued a phase ahead; the first and last ones are
 // gathered by the threads.
+
 constexpr uint64_t kAggReady = 1ull << 63;
 
 template <bool SMALL>
@@ -484,7 +485,14 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
         ctl->words = W0 + tw;
         ctl->distinct = D0 + td;
       }
-      for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) words[W0 + j] = stage[j];
+      {
+        // from a base pointer: one wide multiply-add per address instead
+        // of 64-bit index arithmetic (16-byte funnel-shifted stores measured
+        // slower: 1.035 ms against 0.987 ms on C4)
+        uint32_t* const wd = words + W0;
+#pragma unroll 4
+        for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) wd[j] = stage[j];
+      }
       for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) {
         values[D0 + j] = stage[2 * kEmitTile + j];
         vstart[D0 + j] = uint32_t(W0 + reinterpret_cast<const uint16_t*>(stage + 3 * kEmitTile)[j]);
