@@ -88,7 +88,10 @@ int ndx_memcpy_d2d_async(void* d_dst, const void* d_src, size_t bytes, void* str
  * buffer of ndx_wah_status_bytes(n) bytes owned by the caller, zero-filled
  * ONCE after allocation and used for nothing else: it carries the sort's
  * decoupled look-back statuses, tagged per build so it never needs
- * clearing.  All sizes stay on the device: no stage needs a host round trip.
+ * clearing: its header keeps the tag counter and the high-water mark of the
+ * statuses written, and the build whose 24-bit tags wrap (one in 2^21)
+ * clears them all itself.  All sizes stay on the device: no stage needs a
+ * host round trip.
  * n must be below 2^31 (the index format's word offsets are u32).
  * ------------------------------------------------------------------------- */
 typedef struct {

@@ -294,6 +294,17 @@ __device__ void plan_bytes(Ctl* ctl, uint64_t n, int nbytes) {
     if (s_active[k]) block_excl_scan(ctl->hist_byte[k], p.bucket_start_byte[k], 256);
 }
 
+// Status buffer: [256 B header: u32 epoch counter, u32 pad, u64 high-water
+// mark][statuses of the pass with the most: wide tiles x 2048 digits or byte
+// tiles x 256 digits]
+__host__ __device__ inline uint64_t status_bytes(uint64_t n) {
+  const uint64_t tw = (n + Shape<kWideMaxBits>::TILE - 1) / Shape<kWideMaxBits>::TILE;
+  const uint64_t tb = (n + Shape<8>::TILE - 1) / Shape<8>::TILE;
+  const uint64_t w = tw * kWideBuckets, b = tb * 256;
+  return 256 + (w > b ? w : b) * sizeof(uint64_t);
+}
+constexpr uint32_t kEpochStep = 8, kEpochMax = 0xfffff8u;  // 24-bit tags, 8 per build
+
 // stage 0: after k_hist; stage 1: after k_hist_hi (no-op unless pending).
 // `epoch_counter` lives in the status buffer's header; every build takes a
 // fresh tag so statuses of earlier builds never read as ready.
@@ -305,12 +316,19 @@ __global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage,
     plan_bytes(ctl, n, 4);
     return;
   }
-  __shared__ uint32_t s_mode;
+  __shared__ uint32_t s_mode, s_wrap;
   __shared__ uint32_t rot[kWideBuckets];
   const uint32_t mn = ~ctl->max_not, mx = ctl->max_seen;
+  // The tags are 24 bits: after 2^21 builds they come round again, and a
+  // status left by a build one cycle ago (at tiles no build since has
+  // reached) would read as ready.  So on the wrap every status ever written
+  // -- below the high-water mark kept in the header -- is cleared first.
+  uint64_t* hwm = reinterpret_cast<uint64_t*>(epoch_counter) + 1;
   if (threadIdx.x == 0) {
-    uint32_t ep = (*epoch_counter + 8u) & 0xfffff8u;
-    if (ep == 0) ep = 8;
+    *hwm = umax(*hwm, status_bytes(n));
+    const uint32_t old = *epoch_counter;
+    s_wrap = old >= kEpochMax;
+    const uint32_t ep = old >= kEpochMax ? kEpochStep : old + kEpochStep;
     *epoch_counter = ep;
     ctl->epoch = ep;
     ctl->min_key = mn;
@@ -334,6 +352,11 @@ __global__ __launch_bounds__(1024) void k_plan(Ctl* ctl, uint64_t n, int stage,
     s_mode = p.mode;
   }
   __syncthreads();
+  if (s_wrap) {  // once per 2^21 builds: every status ever written, cleared
+    uint4* q = reinterpret_cast<uint4*>(reinterpret_cast<char*>(epoch_counter) + 256);
+    const uint64_t nq = (*hwm - 256) / sizeof(uint4);
+    for (uint64_t i = threadIdx.x; i < nq; i += blockDim.x) q[i] = make_uint4(0, 0, 0, 0);
+  }
   if (s_mode == kModeWide) {
     const uint32_t nb = 1u << p.wide_bits;
     for (uint32_t d = threadIdx.x; d < uint32_t(kWideBuckets); d += blockDim.x)
@@ -950,12 +973,6 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, uint32_t* epo
   return cudaGetLastError();
 }
 
-// Status buffer: [256 B header: u32 epoch counter][statuses of the pass with
-// the most: wide tiles x 2048 digits or byte tiles x 256 digits]
-static size_t status_bytes(uint64_t n) {
-  const uint64_t w = sort_tiles<kWideMaxBits>(n) * kWideBuckets, b = sort_tiles<8>(n) * 256;
-  return 256 + size_t(umax(w, b)) * sizeof(uint64_t);
-}
 
 }  // namespace ndx
 

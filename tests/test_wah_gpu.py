@@ -220,3 +220,29 @@ def test_largest_workload_digest(w):
     got = b.build(v)
     assert got.words.size == w["W"] and len(got.entries) == w["D"]
     assert "%016x" % oracle.Port().digest_parts(got.row_count, got.entries, got.words) == w["digest"]
+
+
+@pytest.mark.gpu
+def test_epoch_wrap_clears_stale_statuses(port):
+    """The look-back tags are 24 bits and come round after 2^21 builds.  A
+    build that wraps must not be able to read statuses left by the build one
+    cycle earlier at tiles no build has reached since: the wrapping build
+    clears every status below the buffer's high-water mark."""
+    from paper_1709_07781_b200 import ndx
+
+    n = 1 << 21
+    b = ndx.WahBuilder(n)
+    L = b.lib
+    first = gen.zipf(3, n, 65536, 1.0)
+    assert same(b.build(first), port.reference_index(first))
+    assert int(b.status[0].item()) == 8  # the first build's epoch
+    hi = L.ndx_wah_status_bytes(n) // 4
+    assert int(b.status[64:hi].count_nonzero().item()) > 0  # statuses of many tiles
+    b.status[0] = 0xFFFFF8               # the last epoch of the cycle
+    small = gen.zipf(4, 5000, 65536, 1.0)
+    assert same(b.build(small), port.reference_index(small))
+    assert int(b.status[0].item()) == 8  # wrapped: the first build's tags again
+    lo = L.ndx_wah_status_bytes(small.size) // 4
+    assert int(b.status[lo:hi].count_nonzero().item()) == 0  # no stale status left
+    second = gen.zipf(5, n, 65536, 1.0)
+    assert same(b.build(second), port.reference_index(second))
