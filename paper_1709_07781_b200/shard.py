@@ -12,7 +12,9 @@ straddles two ranks), then:
      C++, replicated): merged (value, offset, length) table and, per local
      value, where its words go and which end words change;
   4. the words are gathered to rank 0 (point-to-point over NVLink) and
-     ndx_wah_assemble copies every piece into place.
+     ndx_wah_assemble copies every piece into place; or (exchange_owned)
+     one all-to-all-v by value-range ownership leaves every rank a
+     contiguous slice of the merged word array.
 
 The result on rank 0 is bit-identical to a single-device build of the whole
 column.  No data-path work runs on the host: step 3 touches only metadata.
@@ -295,11 +297,99 @@ def assemble(staged: list, pieces: list[np.ndarray], total_words: int, device, o
     return out[:total_words]
 
 
-def build_distributed(values_local: np.ndarray, row_base: int, builder: ShardBuilder, group=None):
+# ---------------------------------------------------------------------------
+# Owned slices: all-to-all-v by value range
+
+def owner_bounds(entries: np.ndarray, total_words: int, shards: int) -> np.ndarray:
+    """Word bounds b_0..b_G of the slices each rank owns, cut at value
+    boundaries: b_h = offset of the first value whose offset >= h*W/G.  Every
+    piece is one value's words from one shard, so no piece straddles a cut.
+    entries: merged (D,3) u32 table (replicated on every rank)."""
+    off = np.asarray(entries, np.uint32).reshape(-1, 3)[:, 1].astype(np.int64)
+    want = (np.arange(shards + 1, dtype=np.int64) * total_words) // max(shards, 1)
+    idx = np.searchsorted(off, want[1:-1], side="left")
+    inner = np.where(idx < off.size, off[np.minimum(idx, max(off.size - 1, 0))] if off.size else 0, total_words)
+    return np.concatenate([[0], inner, [total_words]]).astype(np.int64)
+
+
+def owned_plan(pieces: list[np.ndarray], bounds: np.ndarray, rank: int):
+    """Host plan of the all-to-all-v, from the replicated merge plan only.
+
+    Returns (pack, send_counts, place, recv_counts):
+      pack   -- this rank's pieces with dst rewritten to packed positions: the
+                assembly writes this rank's final-form words (lead words
+                included) contiguously in global order, i.e. grouped by owner;
+      send_counts[h] -- words of that packed buffer owned by rank h;
+      place  -- pure copies (lead 0) from the received buffer (sources
+                concatenated in rank order) to positions inside the owned
+                slice [bounds[rank], bounds[rank+1]);
+      recv_counts[g] -- words rank g sends here."""
+    G = len(pieces)
+    send_counts = np.zeros((G, G), np.int64)  # [src, dst]
+    owners, plens = [], []
+    for g, p in enumerate(pieces):
+        pl = p["src_len"].astype(np.int64) + (p["lead"] != 0)
+        dst = p["dst"].astype(np.int64)
+        own = np.searchsorted(bounds, dst, side="right") - 1
+        if p.size and (np.any(np.diff(dst) < 0) or np.any(dst + pl > bounds[np.minimum(own + 1, G)])):
+            raise ValueError("owned_plan: pieces out of order or straddling an owner bound")
+        np.add.at(send_counts[g], np.clip(own, 0, G - 1), pl)
+        owners.append(own)
+        plens.append(pl)
+    me = pieces[rank]
+    pack = me.copy()
+    pl = plens[rank]
+    pack["dst"] = (np.cumsum(pl) - pl).astype(np.uint64)
+    recv_counts = send_counts[:, rank].copy()
+    src_base = np.concatenate([[0], np.cumsum(recv_counts)[:-1]])
+    place = []
+    for g, p in enumerate(pieces):
+        sel = (owners[g] == rank) & (plens[g] > 0)
+        k = plens[g][sel]
+        q = np.zeros(int(sel.sum()), PIECE_DTYPE)
+        q["src_off"] = (src_base[g] + np.cumsum(k) - k).astype(np.uint32)
+        q["src_len"] = k.astype(np.uint32)
+        q["dst"] = (p["dst"][sel].astype(np.int64) - bounds[rank]).astype(np.uint64)
+        place.append(q)
+    place = np.concatenate(place) if place else np.zeros(0, PIECE_DTYPE)
+    return pack, send_counts[rank].copy(), place, recv_counts
+
+
+def alltoallv_words(send, send_counts, recv_counts, group=None):
+    """One all_to_all_single with per-rank split sizes (NCCL over NVLink on
+    GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    out = torch.empty(int(np.sum(recv_counts)), dtype=send.dtype, device=send.device)
+    dist.all_to_all_single(out, send.contiguous(), output_split_sizes=[int(x) for x in recv_counts],
+                           input_split_sizes=[int(x) for x in send_counts], group=group)
+    return out
+
+
+def exchange_owned(words_local, entries: np.ndarray, pieces: list[np.ndarray], total_words: int, group=None):
+    """SURVEY.md 8(e) step 3 on the GPU: pack this rank's final-form words
+    (ndx_wah_assemble), all-to-all-v them by value-range ownership, place the
+    received runs (ndx_wah_assemble).  Returns (bounds, slice): this rank's
+    contiguous slice [bounds[r], bounds[r+1]) of the merged word array."""
+    import torch.distributed as dist
+    rank, G = dist.get_rank(group), dist.get_world_size(group)
+    bounds = owner_bounds(entries, total_words, G)
+    pack, sc, place, rc = owned_plan(pieces, bounds, rank)
+    dev = words_local.device
+    send = assemble([words_local], [pack], int(sc.sum()), dev)
+    recv = alltoallv_words(send, sc, rc, group)
+    mine = int(bounds[rank + 1] - bounds[rank])
+    return bounds, assemble([recv], [place], mine, dev)
+
+
+def build_distributed(values_local: np.ndarray, row_base: int, builder: ShardBuilder, group=None,
+                      owned: bool = False):
     """The whole multi-GPU build for this rank's shard (one process per GPU).
 
     Returns (entries (D,3) u32 numpy, words device tensor) on rank 0 and
-    (entries, None) elsewhere; entries are replicated on every rank."""
+    (entries, None) elsewhere; entries are replicated on every rank.  With
+    owned=True every rank instead gets (entries, (bounds, slice)): its
+    contiguous value-range slice of the merged words (exchange_owned)."""
     import torch
     import torch.distributed as dist
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -308,6 +398,12 @@ def build_distributed(values_local: np.ndarray, row_base: int, builder: ShardBui
     W, D, meta_d = builder.build(keys, n, row_base)
     padded, sizes = exchange_meta_device(meta_d, D, group)
     entries, pieces, _, total = plan_merge_device(padded, sizes)
+    if owned:
+        G, cap = padded.shape[0], padded.shape[1] // 8
+        hp = pieces.cpu().numpy().view(PIECE_DTYPE)[: G * cap].reshape(G, cap)
+        ent = entries.cpu().numpy().view(np.uint32)
+        plist = [hp[g, : int(sizes[g])].copy() for g in range(G)]
+        return ent, exchange_owned(builder.words[:W], ent, plist, total, group)
     staged = gather_words(builder.words[:W], dst=0, group=group)
     ent = entries.cpu().numpy().view(np.uint32)
     if dist.get_rank(group) != 0:

@@ -151,3 +151,89 @@ def test_query_chunk_helpers_round_trip():
         c = query.bits_to_chunks(b)
         assert c.size == (n + 30) // 31 and (c < (1 << 31)).all()
         assert np.array_equal(query.chunks_to_bits(c, n), b)
+
+
+def _local_parts(port, v, g):
+    b = shard.shard_bounds(v.size, g).astype(np.int64)
+    metas, words = [], []
+    for k in range(g):
+        part = v[b[k]:b[k + 1]]
+        if part.size == 0:
+            metas.append(np.zeros(0, shard.META_DTYPE))
+            words.append(np.zeros(0, np.uint32))
+            continue
+        e, w = H.local_index(port, part, int(b[k]))
+        metas.append(H.local_meta(part, int(b[k]), e, w))
+        words.append(w)
+    entries, pieces, total = shard.plan_merge(metas)
+    return words, entries.copy(), [p.copy() for p in pieces], total
+
+
+@pytest.mark.parametrize("g", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("name", sorted(H.columns()))
+def test_owned_slices_tile_the_whole_index(port, name, g):
+    """All-to-all-v by value range, the exchange
+    simulated by slicing: every rank's owned slice, concatenated in rank
+    order, is the reference index's word array."""
+    v = H.columns()[name]
+    words, entries, pieces, total = _local_parts(port, v, g)
+    bounds = shard.owner_bounds(entries, total, g)
+    assert bounds[0] == 0 and bounds[-1] == total and np.all(np.diff(bounds) >= 0)
+    assert set(bounds[1:-1].tolist()) <= set(entries[:, 1].tolist()) | {total}  # cuts at value starts
+    plans = [shard.owned_plan(pieces, bounds, r) for r in range(g)]
+    sends = []
+    for r, (pack, sc, place, rc) in enumerate(plans):
+        sends.append(np.split(H.assemble([words[r]], [pack], int(sc.sum())), np.cumsum(sc)[:-1]))
+    out = []
+    for r, (pack, sc, place, rc) in enumerate(plans):
+        recv = np.concatenate([sends[s][r] for s in range(g)])
+        assert recv.size == int(rc.sum())
+        out.append(H.assemble([recv], [place], int(bounds[r + 1] - bounds[r])))
+    assert np.array_equal(np.concatenate(out), port.reference_index(v).words), (name, g)
+
+
+def _owned_worker(rank, ws, port_num, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        import oracle
+
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port_num)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        port = oracle.Port()
+        v = np.concatenate([H.columns()["hot_cold"], H.columns()["ones_across"]])
+        b = shard.shard_bounds(v.size, ws).astype(np.int64)
+        part = v[b[rank]:b[rank + 1]]
+        e, w = H.local_index(port, part, int(b[rank]))
+        metas = shard.exchange_meta(H.local_meta(part, int(b[rank]), e, w))
+        entries, pieces, total = shard.plan_merge(metas)
+        bounds = shard.owner_bounds(entries, total, ws)
+        pack, sc, place, rc = shard.owned_plan(pieces, bounds, rank)
+        send = torch.from_numpy(H.assemble([w], [pack], int(sc.sum())).view(np.int32).copy())
+        recv = shard.alltoallv_words(send, sc, rc).numpy().view(np.uint32)
+        mine = H.assemble([recv], [place], int(bounds[rank + 1] - bounds[rank]))
+        ref = port.reference_index(v).words[bounds[rank]:bounds[rank + 1]]
+        q.put(bool(np.array_equal(mine, ref) and mine.size > 0))
+        dist.destroy_process_group()
+    except Exception as ex:  # pragma: no cover - reported through the queue
+        q.put(repr(ex))
+
+
+def test_owned_slices_alltoallv_gloo_world2():
+    import socket
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port_num = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_owned_worker, args=(r, 2, port_num, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [True, True], res
