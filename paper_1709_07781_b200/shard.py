@@ -333,7 +333,7 @@ def owned_plan(pieces: list[np.ndarray], bounds: np.ndarray, rank: int):
         own = np.searchsorted(bounds, dst, side="right") - 1
         if p.size and (np.any(np.diff(dst) < 0) or np.any(dst + pl > bounds[np.minimum(own + 1, G)])):
             raise ValueError("owned_plan: pieces out of order or straddling an owner bound")
-        np.add.at(send_counts[g], np.clip(own, 0, G - 1), pl)
+        send_counts[g] = np.bincount(np.clip(own, 0, G - 1), weights=pl, minlength=G).astype(np.int64)
         owners.append(own)
         plens.append(pl)
     me = pieces[rank]
