@@ -253,25 +253,34 @@ def run_sharded(args, cfg, world, rank, local):
     gather_ms = max_over_ranks((time.perf_counter() - g0) * 1e3)
 
     # owned slices: all-to-all-v by value range, every
-    # rank ends with a contiguous slice of the merged word array
-    cap, sizes = state["cap"], state["sizes"]
-    hp = state["pieces"].cpu().numpy().view(shard.PIECE_DTYPE)[: world * cap].reshape(world, cap)
-    plist = [hp[g, : int(sizes[g])].copy() for g in range(world)]
-    ent = state["entries"].cpu().numpy().view(np.uint32)
-    shard.exchange_owned(sb.words[: state["W"]], ent, plist, state["total"])  # warm (NCCL p2p setup)
-    barrier()
-    o0 = time.perf_counter()
-    reps = 3
-    for _ in range(reps):
-        obounds, owned = shard.exchange_owned(sb.words[: state["W"]], ent, plist, state["total"])
-    barrier()
-    owned_ms = max_over_ranks((time.perf_counter() - o0) * 1e3 / reps)
-    owned_ok = True
-    if rank == 0:  # rank 0's slice against the gathered index
-        owned_ok = bool(torch.equal(owned, out[int(obounds[0]):int(obounds[1])]))
-    ok_t = torch.tensor([1 if owned_ok else 0], device=dev)
-    dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
-    owned_ok = bool(ok_t.item())
+    # rank ends with a contiguous slice of the merged word array.  Reported
+    # beside the step; a failure is recorded in the line, not fatal (the plan
+    # is replicated, so every rank fails alike and none waits on the others).
+    try:
+        cap, sizes = state["cap"], state["sizes"]
+        hp = state["pieces"].cpu().numpy().view(shard.PIECE_DTYPE)[: world * cap].reshape(world, cap)
+        plist = [hp[g, : int(sizes[g])].copy() for g in range(world)]
+        ent = state["entries"].cpu().numpy().view(np.uint32)
+        shard.exchange_owned(sb.words[: state["W"]], ent, plist, state["total"])  # warm (NCCL p2p setup)
+        barrier()
+        o0 = time.perf_counter()
+        reps = 3
+        for _ in range(reps):
+            obounds, owned = shard.exchange_owned(sb.words[: state["W"]], ent, plist, state["total"])
+        barrier()
+        owned_ms = max_over_ranks((time.perf_counter() - o0) * 1e3 / reps)
+        owned_ok = True
+        if rank == 0:  # rank 0's slice against the gathered index
+            owned_ok = bool(torch.equal(owned, out[int(obounds[0]):int(obounds[1])]))
+        ok_t = torch.tensor([1 if owned_ok else 0], device=dev)
+        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        owned_ok = bool(ok_t.item())
+        owned_info = {"ms": owned_ms, "what": "all-to-all-v of the final-form words by value-range "
+                      "ownership (pack, NCCL all_to_all_single, place); host-planned from the "
+                      "replicated merge plan, after one warm call, mean of 3 beside the step",
+                      "max_slice_words": int(np.max(np.diff(obounds))), "check_ok": owned_ok}
+    except Exception as ex:  # noqa: BLE001 - reported in the JSON line
+        owned_info = {"error": repr(ex)[:200]}
 
     # end to end: pinned host keys in, every step; the rank's merged table and
     # its own words back to the host
@@ -300,10 +309,7 @@ def run_sharded(args, cfg, world, rank, local):
                            "each of its words goes); the gather of all words to rank 0 is timed "
                            "separately"},
         "gather_to_rank0_ms": gather_ms,
-        "owned_slices": {"ms": owned_ms, "what": "all-to-all-v of the final-form words by value-range "
-                         "ownership (pack, NCCL all_to_all_single, place); host-planned from the "
-                         "replicated merge plan, after one warm call, mean of 3 beside the step",
-                         "max_slice_words": int(np.max(np.diff(obounds))), "check_ok": owned_ok},
+        "owned_slices": owned_info,
         "e2e": {"value": total_values / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
                 "d2h_bytes_per_step": 4 * state["W"], "ms_per_step": e2e_ms},
         "gpu_launches": 13 * K,
