@@ -108,3 +108,35 @@ def test_owned_slices_on_gpu(port, name, g):
         out.append(shard.assemble([recv], [place], int(bounds[r + 1] - bounds[r]), torch.device("cuda")))
     got = torch.cat(out).cpu().numpy().view(np.uint32)
     assert np.array_equal(got, port.reference_index(v).words), (name, g)
+
+
+@pytest.mark.parametrize("owned", [False, True])
+def test_build_distributed_world1_nccl(port, owned):
+    """build_distributed end to end through torch.distributed (NCCL, world
+    size 1: one process, nothing waits on another rank): the gathered index
+    and the owned slice both equal the reference's."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port_num = s.getsockname()[1]
+    s.close()
+    store = dist.TCPStore("127.0.0.1", port_num, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        v = gen.zipf(42, 1 << 20, 65536, 1.0)
+        sb = shard.ShardBuilder(v.size)
+        ent, res = shard.build_distributed(v, 0, sb, owned=owned)
+        ref = port.reference_index(v)
+        assert np.array_equal(ent, ref.entries)
+        if owned:
+            bounds, words = res
+            assert bounds.tolist() == [0, ref.words.size]
+        else:
+            words = res
+        assert np.array_equal(words.cpu().numpy().view(np.uint32), ref.words)
+    finally:
+        dist.destroy_process_group()
