@@ -79,6 +79,9 @@ namespace ndx {
 #define NDX_SORT_ATOMRANK 0
 #endif
 // wide keys: two ranks (< 2^16) per register, 16 fewer live registers
+#ifndef NDX_SORT_RANK_BCAST
+#define NDX_SORT_RANK_BCAST 2  // 0 never, 1 every pass, 2 the wide pass only
+#endif
 #ifndef NDX_SORT_PACK_RANK
 #define NDX_SORT_PACK_RANK 1
 #endif
@@ -664,9 +667,19 @@ __device__ __forceinline__ void tile_pass(const TileCtx& t, uint64_t tile, uint3
     old = __shfl_sync(kFull, old, leader);
     const uint32_t rk = old + __popc(peers & lanemask_lt());
 #else
+    // wide pass: every lane reads its digit's counter (peers read one
+    // address: a broadcast), so no shuffle sits in the round-to-round chain
+    // (C3 sort 541 -> 534 us); byte passes keep the leader read + shuffle,
+    // which measured faster there (C4 sort 2.755 vs 2.790 ms)
+    constexpr bool kBcast = NDX_SORT_RANK_BCAST == 1 || (NDX_SORT_RANK_BCAST == 2 && SH::kWide);
     uint32_t old = 0;
-    if (lane == leader) old = Hw[d];
-    old = __shfl_sync(kFull, old, leader);
+    if constexpr (kBcast) {
+      old = Hw[d];
+      __syncwarp();
+    } else {
+      if (lane == leader) old = Hw[d];
+      old = __shfl_sync(kFull, old, leader);
+    }
     if (valid && lane == leader) Hw[d] = uint16_t(old + __popc(peers));
     const uint32_t rk = old + __popc(peers & lanemask_lt());
     __syncwarp();
