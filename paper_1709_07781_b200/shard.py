@@ -326,32 +326,31 @@ def owned_plan(pieces: list[np.ndarray], bounds: np.ndarray, rank: int):
       recv_counts[g] -- words rank g sends here."""
     G = len(pieces)
     send_counts = np.zeros((G, G), np.int64)  # [src, dst]
-    owners, plens = [], []
+    ranges = []
     for g, p in enumerate(pieces):
-        pl = p["src_len"].astype(np.int64) + (p["lead"] != 0)
-        dst = p["dst"].astype(np.int64)
+        a = np.ascontiguousarray(p).view(np.uint32).reshape(-1, 6)  # dst lo, dst hi, off, len, lead, pad
+        dst = a[:, 0].astype(np.int64) | (a[:, 1].astype(np.int64) << 32)
+        pl = a[:, 3].astype(np.int64) + (a[:, 4] != 0)
         own = np.searchsorted(bounds, dst, side="right") - 1
-        if p.size and (np.any(np.diff(dst) < 0) or np.any(dst + pl > bounds[np.minimum(own + 1, G)])):
+        if a.shape[0] and (np.any(np.diff(dst) < 0) or own[0] < 0 or np.any(dst + pl > bounds[np.minimum(own + 1, G)])):
             raise ValueError("owned_plan: pieces out of order or straddling an owner bound")
-        send_counts[g] = np.bincount(np.clip(own, 0, G - 1), weights=pl, minlength=G).astype(np.int64)
-        owners.append(own)
-        plens.append(pl)
-    me = pieces[rank]
-    pack = me.copy()
-    pl = plens[rank]
-    pack["dst"] = (np.cumsum(pl) - pl).astype(np.uint64)
+        cum = np.concatenate([[0], np.cumsum(pl)])
+        cut = np.searchsorted(own, np.arange(G + 1), side="left")  # owners ascend with dst
+        send_counts[g] = np.diff(cum[cut])
+        if g == rank:
+            pack = np.ascontiguousarray(p).copy()
+            pack["dst"] = cum[:-1].astype(np.uint64)
+        lo, hi = int(cut[rank]), int(cut[rank + 1])
+        ranges.append((dst[lo:hi], pl[lo:hi]))
     recv_counts = send_counts[:, rank].copy()
-    src_base = np.concatenate([[0], np.cumsum(recv_counts)[:-1]])
-    place = []
-    for g, p in enumerate(pieces):
-        sel = (owners[g] == rank) & (plens[g] > 0)
-        k = plens[g][sel]
-        q = np.zeros(int(sel.sum()), PIECE_DTYPE)
-        q["src_off"] = (src_base[g] + np.cumsum(k) - k).astype(np.uint32)
-        q["src_len"] = k.astype(np.uint32)
-        q["dst"] = (p["dst"][sel].astype(np.int64) - bounds[rank]).astype(np.uint64)
-        place.append(q)
-    place = np.concatenate(place) if place else np.zeros(0, PIECE_DTYPE)
+    dst = np.concatenate([r[0] for r in ranges]) if G else np.zeros(0, np.int64)
+    k = np.concatenate([r[1] for r in ranges]) if G else np.zeros(0, np.int64)
+    keep = k > 0
+    off = np.cumsum(k) - k  # sources concatenated in rank order
+    place = np.zeros(int(keep.sum()), PIECE_DTYPE)
+    place["src_off"] = off[keep].astype(np.uint32)
+    place["src_len"] = k[keep].astype(np.uint32)
+    place["dst"] = (dst[keep] - bounds[rank]).astype(np.uint64)
     return pack, send_counts[rank].copy(), place, recv_counts
 
 
