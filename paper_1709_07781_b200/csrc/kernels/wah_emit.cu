@@ -41,6 +41,9 @@ constexpr int kEmitWarps = kEmitThreads / 32;
 // 14 pairs per thread: 112-byte thread stride, so the 16-byte shared loads
 // of a quarter warp hit 8 distinct bank groups (8 pairs -> 64 B stride was a
 // 4-way conflict; measured C4 emit 1.49 -> 1.00 ms).  Must be even and < 31.
+#ifndef NDX_EMIT_L2PF
+#define NDX_EMIT_L2PF 0
+#endif
 #ifndef NDX_EMIT_K
 #define NDX_EMIT_K 14
 #endif
@@ -431,6 +434,13 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       const uint32_t nt = has ? atomicAdd(ctr, 1u) : ntiles;
       s_tile[b ^ 1] = nt;
       if (nt < ntiles && by_bulk(nt)) bulk_fill(nt, b ^ 1);
+#if NDX_EMIT_L2PF
+      // the tile one CTA round ahead into L2 (as in the sort's tile loop)
+      const uint64_t pf = uint64_t(nt) + gridDim.x;
+      if (nt < ntiles && (pf + 1) * kEmitTile <= n)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pairs + pf * kEmitTile),
+                     "r"(uint32_t(kEmitTile * 8)) : "memory");
+#endif
     }
 
     if (pending >= 0) {
