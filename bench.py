@@ -66,6 +66,52 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def b_alg(n, W, D, passes):
+    """algorithmic bytes of a build, (8 + 16 P) N + 4 W + 12 D."""
+    return (8 + 16 * passes) * n + 4 * W + 12 * D
+
+
+def b_min(n, W, D):
+    """The compulsory floor: read the keys, write words + table."""
+    return 4 * n + 4 * W + 12 * D
+
+
+def golden_digest(cfg, n):
+    """The reference's digest of this workload (tests/golden/digests.json,
+    generated from oracle/_ref), or None when no fixture covers it."""
+    p = os.path.join(ROOT, "tests", "golden", "digests.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+    except OSError:
+        return None
+    for w in d.get("workloads", []) + d.get("gpu_workloads", []):
+        if (w["kind"], w["seed"], w["n"], w["k"]) == (cfg["kind"], cfg["seed"], n, cfg["k"]):
+            return w["digest"]
+    return None
+
+
+def device_result_digest(n, d_counts, d_words, d_entries):
+    """Digest of an index left in HBM by the actor chain: counts, words and
+    table copied to the host, FNV-1a-64 of the WAH1 bytes in native code."""
+    from paper_1709_07781_b200 import ndx
+    from paper_1709_07781_b200.runtime import index_digest
+
+    L = ndx.load()
+    c = np.zeros(4, np.uint64)
+    ndx.check(L.ndx_memcpy_d2h_async(c.ctypes.data, d_counts, 24, None), "d2h counts")
+    ndx.check(L.ndx_device_synchronize(), "sync")
+    W, D = int(c[0]), int(c[1])
+    w = np.empty(max(W, 1), np.uint32)
+    e = np.empty(max(3 * D, 1), np.uint32)
+    if W:
+        ndx.check(L.ndx_memcpy_d2h_async(w.ctypes.data, d_words, 4 * W, None), "d2h words")
+    if D:
+        ndx.check(L.ndx_memcpy_d2h_async(e.ctypes.data, d_entries, 12 * D, None), "d2h entries")
+    ndx.check(L.ndx_device_synchronize(), "sync")
+    return "%016x" % index_digest(n, e[: 3 * D], w[:W]), W, D
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 50 ms during the
     timed region (nvidia-smi -lms in the background)."""
@@ -118,11 +164,26 @@ def dist_setup(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        os.environ["NCCL_DEBUG"] = "WARN"  # stdout carries exactly one JSON line
+        # communicator lines on stderr (stdout carries exactly one JSON line)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if args.impl == "ours":
             torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo", rank=rank, world_size=world)
     return world, rank, local
+
+
+def ref_values(cfg, n, rank=0):
+    """The same synthetic stream from the reference's own generators
+    (oracle/_ref: libstdc++ distributions), so the CPU legs never load the
+    product libraries; the C restatement's stream when oracle/_ref is absent."""
+    import oracle
+
+    seed = cfg["seed"] + rank
+    if oracle.Reference.available():
+        r = oracle.Reference()
+        return r.gen_zipf(seed, n, cfg["k"], 1.0) if cfg["kind"] == "zipf" else r.gen_uniform(seed, n, cfg["k"])
+    raise RuntimeError("oracle/_ref/libndref.so missing: build it with make -C oracle")
 
 
 def cpu_baseline(cfg):
@@ -130,7 +191,7 @@ def cpu_baseline(cfg):
     import oracle
 
     n = 1 << 25
-    v = gen_values(cfg, n, 0)
+    v = ref_values(cfg, n)
     if oracle.Reference.available():
         impl, kind = oracle.Reference(), "reference"
     else:
@@ -143,24 +204,38 @@ def cpu_baseline(cfg):
                       f"({dt:.1f} s)"}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, cfg):
+    """The reference's own data-parallel CPU build, wah::build_index on its
+    simulated device (p/core/src/wah_builder.cpp:38-307), compiled from the
+    reference sources into oracle/_ref.  Inputs come from the reference's
+    generators; nothing of the product package is imported or loaded."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return 0
     import oracle
 
     n = args.ref_sample
-    v = gen_values(cfg, n, 0)
+    v = ref_values(cfg, n)
     cores = os.cpu_count() or 1
-    if oracle.Reference.available():
-        build = lambda: oracle.Reference().build_index_sim(v, cores, 8)  # noqa: E731
-        kind = "reference"
-        what = f"wah::build_index on the reference's simulated device, {cores} compute units, 8-bit digits"
-    else:
-        build = lambda: oracle.Port().reference_index(v)  # noqa: E731
-        kind = "port"
-        what = "C restatement of wah::reference_index, 1 thread"
-        cores = 1
+    if not oracle.Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libndref.so was not built"}))
+        return 0
+    ref = oracle.Reference()
+    # BASELINE.md section 3: all host threads as compute units, 8-bit digits
+    # at N >= 2^26 (16-bit digits need 4N-entry histograms per pass)
+    build = lambda: ref.build_index_sim(v, cores, 8)  # noqa: E731
+    what = f"wah::build_index on the reference's simulated device, {cores} compute units, 8-bit digits"
     for _ in range(args.warmup):
         build()
     times = []
@@ -168,15 +243,17 @@ def run_reference(args, cfg):
         t0 = time.perf_counter()
         build()
         times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
+    t = statistics.median(times)
     value = n / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "sample_values_per_step": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{what}; {n} values of the same stream per step"},
+        "config": {"workload": cfg["desc"], "sample_values_per_step": n,
+                   "sample": f"first {n} values of the config's stream (reference generator)",
+                   "cpu": cpu_model(), "nproc": cores},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{what}; the first {n} values of the same stream per step, median of {args.steps}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -337,11 +414,13 @@ def extra_config(rt, raw, dev, K, W_, name="C3"):
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a0.record(rts)
     for _ in range(K):
-        rt.build_index_device(keys.data_ptr(), n)
+        ptrs = rt.build_index_device(keys.data_ptr(), n)
     rt.synchronize()  # every stage issued (actor hops, launcher ring) and done
     a1.record(rts)
     a1.synchronize()
     ms = a0.elapsed_time(a1) / K
+    dg, _, _ = device_result_digest(n, *ptrs)
+    want = golden_digest(c, n)
     stream = torch.cuda.current_stream()
     calls = raw.stage_calls(keys, n, row_base=0, stream=stream)
     for _, cl in calls:
@@ -356,8 +435,12 @@ def extra_config(rt, raw, dev, K, W_, name="C3"):
     stage_ms = {nm: sum(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(K)) / K
                 for i, (nm, _) in enumerate(calls)}
     W, D = raw.counts()
+    raw_ms = sum(stage_ms.values())
     return {"workload": c["desc"], "value": n / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
-            "stage_ms": stage_ms, "words": W, "distinct": D, "data": "synthetic (mt19937(1), uniform)"}
+            "stage_ms": stage_ms, "raw_launch_ms": raw_ms, "chain_overhead_vs_raw": ms / raw_ms - 1.0,
+            "gbs_alg": b_alg(n, W, D, 1) / (ms * 1e-3) / 1e9,
+            "words": W, "distinct": D, "data": "synthetic (mt19937(1), uniform)",
+            "result_digest": dg, "golden_digest": want, "result_check_ok": want is not None and dg == want}
 
 
 def run_ours(args, cfg):
@@ -417,7 +500,7 @@ def run_ours(args, cfg):
     a1 = torch.cuda.Event(enable_timing=True)
     a0.record(rts)
     for _ in range(K):
-        rt.build_index_device(keys.data_ptr(), n)
+        ptrs = rt.build_index_device(keys.data_ptr(), n)
     # the requests return once queued: the stages reach the stream through
     # the actor hops and the launcher thread, so the end event is recorded
     # only after everything was issued and has finished
@@ -426,6 +509,11 @@ def run_ours(args, cfg):
     barrier()
     a1.synchronize()
     ms = max_over_ranks(a0.elapsed_time(a1) / K)
+
+    # ---- content check of the headline result (the actor chain's index in
+    #      HBM) against the reference's digest of this workload
+    chain_digest, _, _ = device_result_digest(n, *ptrs)
+    want_digest = golden_digest(cfg, n)
 
     # ---- the same four stages launched raw through the C ABI (per-stage events)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(K)]
@@ -477,9 +565,14 @@ def run_ours(args, cfg):
     for tk in pend:
         rt.wait(tk)
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
-    W_e2e, D_e2e = int(hc[(e2e_steps - 1) % 2][0]), int(hc[(e2e_steps - 1) % 2][1])
+    last = (e2e_steps - 1) % 2
+    W_e2e, D_e2e = int(hc[last][0]), int(hc[last][1])
     d2h = 24 + 4 * W_e2e + 12 * D_e2e
-    e2e_ok = W_e2e == W and D_e2e == D and 3 * D_e2e <= ecap
+    from paper_1709_07781_b200.runtime import index_digest
+
+    e2e_digest = "%016x" % index_digest(n, he[last][: 3 * D_e2e], hw[last][:W_e2e])
+    e2e_ok = 3 * D_e2e <= ecap and (e2e_digest == want_digest if want_digest else
+                                    (W_e2e == W and D_e2e == D and e2e_digest == chain_digest))
     t0 = time.perf_counter()
     rt.build_index(hk, hw[0], he[0])
     e2e_sync_ms = (time.perf_counter() - t0) * 1e3
@@ -509,6 +602,7 @@ def run_ours(args, cfg):
         with open(tp) as f:
             traffic = json.load(f).get(args.config, {}).get(dom)
 
+    ba, bm = b_alg(n, W, D, 2), b_min(n, W, D)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W_, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -518,6 +612,14 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (4 B keys x values per GPU > 126 MB)",
                    "parallelism": f"row shards x{world}", "words": W, "distinct": D,
                    "path": "compute-actor chain table*emit*sort*plan over device MemRefs"},
+        "result_check": {"what": "FNV-1a-64 of the WAH1 bytes of the actor chain's index (HBM, last timed "
+                                 "step) against the reference's digest (tests/golden/digests.json)",
+                         "digest": chain_digest, "golden": want_digest,
+                         "ok": want_digest is not None and chain_digest == want_digest},
+        "build_gbs": {"b_alg_bytes": ba, "gbs_alg": ba / (ms * 1e-3) / 1e9,
+                      "frac_alg": ba / (ms * 1e-3) / 1e9 / peak, "frac_alg_spec_8tbs": ba / (ms * 1e-3) / 8e12,
+                      "b_min_bytes": bm, "gbs_effective": bm / (ms * 1e-3) / 1e9,
+                      "model": "SURVEY 8(d): B_alg = 40N + 4W + 12D (2-pass LSD model), B_min = 4N + 4W + 12D"},
         "stage_ms": stage_ms,
         "dispatch": {"chain_ms": ms, "raw_launch_ms": raw_ms,
                      "chain_overhead_vs_raw": ms / raw_ms - 1.0,
@@ -533,7 +635,7 @@ def run_ours(args, cfg):
         "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": e2e_steps,
                 "pipelined": "2 deep: step i+1 upload (H2D) and build overlap step i result copy (D2H on the copy engines)",
-                "result_check_ok": e2e_ok, "sync_call_ms": e2e_sync_ms},
+                "result_check_ok": e2e_ok, "result_digest": e2e_digest, "sync_call_ms": e2e_sync_ms},
         "gpu_launches": 11 * K,
         "clocks": clk,
     }
@@ -560,7 +662,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
     ap.add_argument("--n", type=int, default=0, help="values per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=16)
-    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--ref-sample", type=int, default=1 << 26)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3 line inside the C4 report")
     ap.add_argument("--force-sharded", action="store_true",

@@ -105,6 +105,12 @@ int ndactor_merge_plan(uint32_t shards, const ndx_shard_meta* metas, const uint6
                        uint64_t stride, uint32_t* entries, ndx_piece* pieces,
                        uint64_t* n_entries, uint64_t* n_words);
 
+/* FNV-1a-64 of the "WAH1" serialization of an index (row_count, entries as
+ * (value, offset, length) triples, words) -- the digest of SURVEY.md App. C
+ * and tests/golden/digests.json, computed without a serialized copy. */
+uint64_t ndactor_index_digest(uint32_t row_count, const uint32_t* entries, uint64_t n_entries,
+                              const uint32_t* words, uint64_t n_words);
+
 /* "WAH1" index file (p/core/src/wah_index_io.cpp:30-87). */
 int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_t* entries,
                              uint64_t n_entries, const uint32_t* words, uint64_t n_words);

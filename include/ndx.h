@@ -43,6 +43,7 @@ int ndx_abi_version(void);
  * ------------------------------------------------------------------------- */
 int ndx_device_count(int* count);
 int ndx_device_open(int ordinal);           /* cudaSetDevice + mempool setup */
+int ndx_device_bind(int ordinal);           /* cudaSetDevice only (per host thread) */
 int ndx_device_sm_count(int ordinal, int* sms);
 int ndx_device_synchronize(void);
 

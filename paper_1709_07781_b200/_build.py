@@ -46,10 +46,12 @@ def build_ndx(force: bool = False) -> str:
     deps = srcs + glob.glob(os.path.join(CSRC, "kernels", "*.cuh")) + [os.path.join(INC, "ndx.h")]
     if force or _stale(out, deps):
         os.makedirs(LIB, exist_ok=True)
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+        # -rdc: the plan and sort stages launch exactly the kernels the
+        # device-made plan needs from the device (tail launches, CDP)
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-rdc=true", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-v" if os.environ.get("NDX_PTXAS_V") else "-O3",
               "--expt-relaxed-constexpr", "-cudart", "static", "-shared", "-I" + INC, *defines,
-              "-o", out, *srcs])
+              "-o", out, *srcs, "-lcudadevrt"])
     return out
 
 

@@ -49,6 +49,8 @@ int ndx_device_open(int ordinal) {
   return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
 }
 
+int ndx_device_bind(int ordinal) { return cudaSetDevice(ordinal); }
+
 int ndx_device_sm_count(int ordinal, int* sms) {
   if (!sms) return NDX_E_INVALID;
   return cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, ordinal);

@@ -7,7 +7,7 @@
 
 namespace ndx {
 
-enum SortMode : uint32_t { kModeNone = 0, kModeWide = 1, kModeBytes = 2 };
+enum SortMode : uint32_t { kModeNone = 0, kModeWide = 1, kModeBytes = 2, kModeAB = 3 };
 
 constexpr int kWideMaxBits = 11;                 // single pass up to 2048 buckets
 constexpr int kWideBuckets = 1 << kWideMaxBits;
@@ -16,12 +16,12 @@ struct SortPlan {
   uint32_t mode;           // SortMode
   uint32_t complete;       // plan final (bytes 2/3 histograms not pending)
   uint32_t need_hi;        // bytes 2/3 vary: second histogram pass required
-  uint32_t base;           // wide mode: digit = key - base
+  uint32_t base;           // wide mode: digit = key - base; compact mode: the keys' top 16 bits
   uint32_t wide_bits;      // wide mode: digit width (0..11)
+  uint32_t nseg;           // compact mode: row segments (2^24 rows each)
   uint32_t npasses;        // number of scatter passes that run
   uint32_t byte_active[4]; // bytes mode: byte k gets a pass
   uint32_t byte_order[4];  // bytes mode: execution index of byte k's pass
-  uint32_t byte_count[4];  // bytes mode: per-chunk histogram of byte k must be counted
   uint32_t bucket_start_wide[kWideBuckets];
   uint32_t bucket_start_byte[4][256];
 };
@@ -38,6 +38,7 @@ struct Ctl {
   uint32_t max_seen;   // max(key)
   uint32_t max_not;    // max(~key) -> min = ~max_not
   uint32_t tile_ctr[16];
+  uint32_t grid_bar[2];  // cooperative sort launch: arrivals, generation
   uint32_t hist_byte[4][256];
   uint32_t hist_wide[kWideBuckets];
   uint32_t zero_end;

@@ -186,6 +186,7 @@ int ndactor_wah_build_index(ndactor_runtime* rt, const uint32_t* values, uint64_
     if (n_words) *n_words = 0;
     if (n_entries) *n_entries = 0;
     if (n == 0) return 0;
+    if (n >= (uint64_t(1) << 31)) throw std::length_error("a build takes at most 2^31 - 1 values");
     if (row_base != 0) throw std::invalid_argument("row_base needs ndactor_wah_build_index_device");
     Device& dev = *rt->dev;
     Buffer keys = dev.create_buffer_uninit(ElemType::u32, std::int64_t(n));
@@ -224,6 +225,7 @@ int ndactor_wah_build_index_async(ndactor_runtime* rt, const uint32_t* values, u
   return guarded([&] {
     if (!rt || !counts || !ticket) throw std::invalid_argument("null argument");
     if (n == 0) throw std::invalid_argument("empty input");
+    if (n >= (uint64_t(1) << 31)) throw std::length_error("a build takes at most 2^31 - 1 values");
     if ((!words && words_cap) || (!entries && entries_cap)) throw std::invalid_argument("null output buffer");
     Device& dev = *rt->dev;
     auto ck = [](int rc, const char* what) {
@@ -323,6 +325,9 @@ int ndactor_wah_build_index_device(ndactor_runtime* rt, const uint32_t* d_keys, 
     if (!rt) throw std::invalid_argument("null runtime");
     rt->last = wah::DeviceIndex{};  // previous result: released in stream order
     if (n == 0) return 0;
+    if (n >= (uint64_t(1) << 31)) throw std::length_error("a build takes at most 2^31 - 1 values");
+    if (uint64_t(row_base) + n > (uint64_t(1) << 32))
+      throw std::length_error("row ids row_base .. row_base + n - 1 must fit in u32");
     Device& dev = *rt->dev;
     wah::IndexStages* st = &rt->stages;
     if (row_base != 0) {
@@ -455,6 +460,28 @@ int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_
     wah::write_index_file(path, idx);
     return 0;
   });
+}
+
+// FNV-1a-64 over the "WAH1" serialization, streamed from the parts (no
+// serialized copy): the digest the parity fixtures and SURVEY App. C use.
+uint64_t ndactor_index_digest(uint32_t row_count, const uint32_t* entries, uint64_t n_entries,
+                              const uint32_t* words, uint64_t n_words) {
+  uint64_t h = 1469598103934665603ull;
+  auto bytes = [&h](const void* p, uint64_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (uint64_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  auto u32 = [&bytes](uint32_t v) {
+    const unsigned char le[4] = {uint8_t(v), uint8_t(v >> 8), uint8_t(v >> 16), uint8_t(v >> 24)};
+    bytes(le, 4);
+  };
+  bytes("WAH1", 4);
+  u32(row_count);
+  u32(uint32_t(n_entries));
+  u32(uint32_t(n_words));
+  if (n_entries) bytes(entries, 12 * n_entries);  // little-endian host
+  if (n_words) bytes(words, 4 * n_words);
+  return h;
 }
 
 int ndactor_shard_bounds(uint64_t n, uint32_t shards, uint64_t* bounds) {

@@ -22,9 +22,26 @@ namespace {
 std::string cuda_msg(int rc) { return ndx_error_string(rc); }
 }  // namespace
 
+// CUDA's current device is per host thread: every thread that touches this
+// Device's stream, events or kernels binds to its ordinal first (cached, so
+// the hot path pays one compare).
+int bind_thread(int ordinal) {
+  thread_local int bound = -1;
+  if (bound == ordinal) return 0;
+  const int rc = ndx_device_bind(ordinal);
+  if (rc == 0) bound = ordinal;
+  return rc;
+}
+
 void DeviceImpl::start() {
-  completer = std::thread([this] { completer_loop(); });
-  launcher = std::thread([this] { launcher_loop(); });
+  completer = std::thread([this] {
+    bind_thread(ordinal);
+    completer_loop();
+  });
+  launcher = std::thread([this] {
+    bind_thread(ordinal);
+    launcher_loop();
+  });
 }
 
 void DeviceImpl::stop() {
@@ -191,7 +208,8 @@ bool DeviceImpl::sync_now() {
     } else {
       drain();
       s = issued;
-      rc = ndx_event_create(&ev, 0);
+      rc = bind_thread(ordinal);
+      if (!rc) rc = ndx_event_create(&ev, 0);
       if (!rc) rc = ndx_event_record(ev, stream);
     }
   }
@@ -221,7 +239,8 @@ void DeviceImpl::poll() {
     std::lock_guard<std::mutex> l(issue_mu);
     if (broken) return;
     s = launched.load(std::memory_order_acquire);  // queued launches are not on the stream yet
-    rc = ndx_stream_query(stream);
+    rc = bind_thread(ordinal);
+    if (!rc) rc = ndx_stream_query(stream);
   }
   if (rc == 0) {
     complete_upto(s);
@@ -290,6 +309,7 @@ void DeviceImpl::block_put(void* p, std::size_t cls) {
   cached_bytes += cls;
   while (cached_bytes > kCacheLimit && !block_cache.empty()) {
     drain();
+    bind_thread(ordinal);
     auto it = std::prev(block_cache.end());  // drop the largest
     ndx_free_async(it->second, stream);
     cached_bytes -= it->first;
@@ -299,6 +319,7 @@ void DeviceImpl::block_put(void* p, std::size_t cls) {
 
 void DeviceImpl::block_trim() {
   drain();
+  bind_thread(ordinal);
   for (auto& kv : block_cache) ndx_free_async(kv.second, stream);
   block_cache.clear();
   cached_bytes = 0;
@@ -311,6 +332,7 @@ void DeviceImpl::pinned_put(void* p, std::size_t cap) {
 
 }  // namespace detail
 
+using detail::bind_thread;
 using detail::DeviceImpl;
 
 namespace {
@@ -342,12 +364,25 @@ void issue_now(const std::shared_ptr<DeviceImpl>& d, const Event& ev, Issue& w) 
     const std::uint64_t want = dep.shared_state()->seq.load(std::memory_order_acquire);
     for (unsigned i = 0; od->launched.load(std::memory_order_acquire) < want; ++i)
       if (i > 256) std::this_thread::yield();
+    // the fence event belongs to the producer's device and is recorded on
+    // its stream; the consumer's stream then waits on it (cross-device wait)
     void* fence = nullptr;
-    if (ndx_event_create(&fence, 0) == 0) {
-      ndx_event_record(fence, od->stream);  // after the dependency on its stream
-      ndx_stream_wait_event(d->stream, fence);
-      ndx_event_destroy(fence);
+    int frc = bind_thread(od->ordinal);
+    if (!frc) frc = ndx_event_create(&fence, 0);
+    if (!frc) frc = ndx_event_record(fence, od->stream);
+    const int brc = bind_thread(d->ordinal);
+    if (!frc) frc = brc;
+    if (!frc) frc = ndx_stream_wait_event(d->stream, fence);
+    if (fence) ndx_event_destroy(fence);
+    if (frc) {
+      detail::finish_event(ev.shared_state(), false,
+                           "kernel " + w.name + ": cross-device fence: " + ndx_error_string(frc));
+      return;
     }
+  }
+  if (const int brc = bind_thread(d->ordinal)) {
+    detail::finish_event(ev.shared_state(), false, "kernel " + w.name + ": " + ndx_error_string(brc));
+    return;
   }
   ev.mark_exec_start();
   const int rc = w.fn(d->stream);

@@ -41,6 +41,10 @@ struct Event::State {
 
 namespace detail {
 
+// Make `ordinal` the calling host thread's current CUDA device (cached per
+// thread); 0 or a CUDA error code.
+int bind_thread(int ordinal);
+
 struct DeviceImpl : std::enable_shared_from_this<DeviceImpl> {
   int ordinal = 0;
   void* stream = nullptr;

@@ -33,6 +33,7 @@ SIGNATURES = [
     ("ndx_abi_version", ctypes.c_int, []),
     ("ndx_device_count", ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     ("ndx_device_open", ctypes.c_int, [ctypes.c_int]),
+    ("ndx_device_bind", ctypes.c_int, [ctypes.c_int]),
     ("ndx_device_sm_count", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("ndx_device_synchronize", ctypes.c_int, []),
     ("ndx_stream_create", ctypes.c_int, [ctypes.POINTER(_vp)]),

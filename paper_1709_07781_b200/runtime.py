@@ -53,6 +53,7 @@ def load() -> ctypes.CDLL:
             "ndactor_merge_plan": (ctypes.c_int, [ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp, ctypes.POINTER(_u64),
                                                   ctypes.POINTER(_u64)]),
             "ndactor_write_index_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, _vp, _u64, _vp, _u64]),
+            "ndactor_index_digest": (_u64, [ctypes.c_uint32, _vp, _u64, _vp, _u64]),
         }
         for name, (rt, args) in sig.items():
             fn = getattr(lib, name)
@@ -60,6 +61,15 @@ def load() -> ctypes.CDLL:
             fn.argtypes = args
         _LIB = lib
     return _LIB
+
+
+def index_digest(row_count: int, entries: np.ndarray, words: np.ndarray) -> int:
+    """FNV-1a-64 of the "WAH1" serialization (SURVEY.md App. C digest), in
+    native code: entries are (value, offset, length) u32 triples."""
+    e = np.ascontiguousarray(entries, dtype=np.uint32).reshape(-1)
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    return int(load().ndactor_index_digest(row_count, e.ctypes.data if e.size else None, e.size // 3,
+                                           w.ctypes.data if w.size else None, w.size))
 
 
 def _check(rc: int, what: str) -> None:

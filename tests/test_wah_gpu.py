@@ -116,6 +116,30 @@ def test_baseline_workload_digests(builder, port, w):
     assert "%016x" % port.digest_parts(got.row_count, got.entries, got.words) == w["digest"]
 
 
+@pytest.mark.parametrize("case", ["compact_high_base", "compact_small_many_groups", "compact_segments",
+                                  "compact_sparse_across_segments", "compact_one_low_byte_bucket"])
+def test_compact_two_pass_mode(builder, port, case):
+    """The compact mode (key range >= 2^11, bytes 2/3 constant, 0/1 varying):
+    pass A's packed u32 carries the row's low 24 bits; pass B recovers the
+    low byte and the row segment from the group tables."""
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
+    if case == "compact_high_base":  # a nonzero constant top half
+        v = (0x12340000 + rng.integers(0, 65536, 300_000)).astype(np.uint32)
+    elif case == "compact_small_many_groups":  # more groups than fit a tile's fast path
+        v = rng.integers(0, 60_000, 5000).astype(np.uint32)
+    elif case == "compact_segments":  # several 2^24-row segments
+        v = rng.integers(0, 65536, (1 << 24) * 2 + 12345).astype(np.uint32)
+    elif case == "compact_sparse_across_segments":  # a key seen once per distant segment
+        v = rng.integers(0, 60_000, (1 << 25) + 100).astype(np.uint32)
+        v[5] = 65535
+        v[(1 << 25) + 3] = 65535
+        v[(1 << 24) + 7] = 65279  # same low byte, another high byte
+    else:  # every key shares its low byte: one pass-A bucket
+        v = (rng.integers(0, 256, 200_000).astype(np.uint32) << 8) | 0x77
+    got = builder.build(v)
+    assert same(got, port.reference_index(v)), case
+
+
 def test_repeat_builds_are_deterministic(builder, port):
     v = gen.uniform(3, 500_000, 300)
     a = builder.build(v)
