@@ -52,7 +52,7 @@ enum PassKind : int { kPassWide = 0, kPassA = 1, kPassB = 2 };
 #define NDX_A_MINB 3
 #endif
 #ifndef NDX_B_MINB
-#define NDX_B_MINB 2
+#define NDX_B_MINB 3  // with NDX_B_ALIAS: 3 CTAs per SM (C4 sort 2.307 vs 2.420 ms at 2)
 #endif
 // input buffer aliased with the staging area (no TMA overlap inside a CTA,
 // half the shared memory, so more CTAs per SM)
@@ -63,7 +63,14 @@ enum PassKind : int { kPassWide = 0, kPassA = 1, kPassB = 2 };
 #define NDX_A_ALIAS 0
 #endif
 #ifndef NDX_B_ALIAS
-#define NDX_B_ALIAS 0
+#define NDX_B_ALIAS 1
+#endif
+// claim the next tile at the end of this one (claim order == processing
+// order, so a tile's predecessors are ahead of it when it looks back), its
+// TMA copy then, and an L2 prefetch of the tile one CTA round further on;
+// 0: claim (and copy) at the start of this tile, a whole tile ahead
+#ifndef NDX_CLAIM_LATE
+#define NDX_CLAIM_LATE 1
 #endif
 // every lane reads its digit's counter (broadcast) instead of leader + shfl
 #ifndef NDX_WIDE_BCAST
@@ -179,8 +186,23 @@ __device__ __forceinline__ void group_starts(const PassCtx& c, int par) {  // wa
 }
 
 // One tile.  FULL: all TILE elements exist (every tile but the last).
+template <int KIND, int BITS>
+__device__ __forceinline__ void claim_next(const PassCtx& c, int par) {  // thread 0
+  constexpr uint32_t TILE = PassShape<KIND>::TILE;
+  const uint32_t nt = atomicAdd(c.ctr, 1u);
+  c.m->tile[par ^ 1] = nt;
+  if (nt >= c.tiles) return;
+  if (!PassShape<KIND>::ALIAS && c.bulk && uint64_t(nt + 1) * TILE <= c.n) issue_tile_copy<KIND, BITS>(c, nt);
+  if (KIND == kPassB) group_words(c, nt, par ^ 1);
+  if (NDX_CLAIM_LATE && c.bulk) {
+    const uint64_t pf = uint64_t(nt) + gridDim.x;  // about one CTA round ahead
+    if ((pf + 1) * TILE <= c.n)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c.src + pf * TILE), "r"(TILE * 4u) : "memory");
+  }
+}
+
 template <int KIND, int BITS, bool FULL>
-__device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int par, uint32_t& phase) {
+__device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int par, uint32_t& phase, bool later) {
   using SH = PassShape<KIND>;
   using Stage = typename SH::Stage;
   constexpr uint32_t NB = 1u << BITS;
@@ -217,13 +239,14 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
     if (KIND == kPassWide) x[r] = (x[r] - c.kbase) & DMASK;  // digit < 2^11; the rank goes above bit 16
     if (KIND == kPassA) x[r] &= 0xffffu;                     // lo | hb << 8; the rank goes above bit 16
   }
-  __syncthreads();  // inbuf consumed; R free (previous scatter done)
-  if (threadIdx.x == 0) {
-    const uint32_t nt = atomicAdd(c.ctr, 1u);
-    m->tile[par ^ 1] = nt;
-    if (!SH::ALIAS && nt < c.tiles && c.bulk && uint64_t(nt + 1) * TILE <= c.n) issue_tile_copy<KIND, BITS>(c, nt);
-    if (KIND == kPassB && nt < c.tiles) group_words(c, nt, par ^ 1);
+  if (NDX_CLAIM_LATE && KIND == kPassB && later && warp == 0) {
+    // this tile's group words were requested at its claim: now its group starts
+    if (lane == 0) cp_async_wait_all();
+    __syncwarp();
+    group_starts(c, par);
   }
+  __syncthreads();  // inbuf consumed; R free (previous scatter done)
+  if (!NDX_CLAIM_LATE && threadIdx.x == 0) claim_next<KIND, BITS>(c, par);
 
   // ---- 2. rank
   uint16_t* Hw = H + warp * NB;
@@ -451,7 +474,9 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
       a.X[gbase[(uint32_t(e) >> 8) & 0xffu] + jj] = e;
     }
   }
-  if (KIND == kPassB && warp == 0 && m->tile[par ^ 1] < c.tiles) {
+  if (NDX_CLAIM_LATE) {
+    if (threadIdx.x == 0) claim_next<KIND, BITS>(c, par);
+  } else if (KIND == kPassB && warp == 0 && m->tile[par ^ 1] < c.tiles) {
     if (lane == 0) cp_async_wait_all();  // tile_group words of the next tile
     __syncwarp();
     group_starts(c, par ^ 1);
@@ -513,9 +538,9 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, int bulk_ok, unsigne
     const uint32_t tile = m->tile[par];
     if (tile >= c.tiles) break;
     if (uint64_t(tile + 1) * SH::TILE <= c.n)
-      tma_tile<KIND, BITS, true>(c, tile, par, phase);
+      tma_tile<KIND, BITS, true>(c, tile, par, phase, it > 0);
     else
-      tma_tile<KIND, BITS, false>(c, tile, par, phase);
+      tma_tile<KIND, BITS, false>(c, tile, par, phase, it > 0);
   }
 }
 
