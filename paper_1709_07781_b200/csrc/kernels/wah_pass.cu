@@ -22,15 +22,24 @@
 //   Bytes per element: wide 12; A + B 8 + 12 = 20 (the u64 ping-pong of
 //   the legacy byte passes, wah_sort.cu, moves 12 + 16 = 28).
 //
-// Per tile (persistent CTAs, tiles taken in order from an atomic counter):
+// The first pass (wide or A) reads the keys in their original order, so
+// its digit offsets per chunk of keys come from the plan stage (k_hist
+// counts every chunk, k_chunk_scan scans the counts): each CTA walks its
+// chunks' tiles in order with running digit offsets in shared memory -- no
+// look-back and no waiting on other CTAs -- and copies its next tile in by
+// TMA while it works on the current one.  Pass B reads pass A's output, so
+// its tiles resolve their digit offsets by a decoupled look-back.
+//
+// Per tile:
 //   1. the tile arrives in shared memory by one TMA bulk copy
-//      (cp.async.bulk + mbarrier), issued while the previous tile was being
-//      ranked; every thread then reads its elements with conflict-free LDS
+//      (cp.async.bulk + mbarrier); every thread reads its elements with
+//      conflict-free LDS
 //   2. warp ballot-match ranking (lane order == row order: stable), per-warp
 //      digit counters in shared memory
-//   3. digit counts published (decoupled look-back status), local scan
+//   3. tile digit counts, local scan; global digit bases from the running
+//      chunk offsets (wide, A) or the look-back (B)
 //   4. staging in shared memory in digit order (u32 for wide/A, the final
-//      pair for B) while the look-back resolves the tile's global bases
+//      pair for B)
 //   5. coalesced scatter of the staged runs
 #include <cuda_runtime.h>
 
@@ -54,8 +63,8 @@ enum PassKind : int { kPassWide = 0, kPassA = 1, kPassB = 2 };
 #ifndef NDX_B_MINB
 #define NDX_B_MINB 3  // with NDX_B_ALIAS: 3 CTAs per SM (C4 sort 2.307 vs 2.420 ms at 2)
 #endif
-// input buffer aliased with the staging area (no TMA overlap inside a CTA,
-// half the shared memory, so more CTAs per SM)
+// input buffer aliased with the staging area (the next tile's copy waits for
+// the end of this one; half the shared memory, so more CTAs per SM)
 #ifndef NDX_WIDE_ALIAS
 #define NDX_WIDE_ALIAS 0
 #endif
@@ -65,25 +74,12 @@ enum PassKind : int { kPassWide = 0, kPassA = 1, kPassB = 2 };
 #ifndef NDX_B_ALIAS
 #define NDX_B_ALIAS 1
 #endif
-// claim the next tile at the end of this one (claim order == processing
-// order, so a tile's predecessors are ahead of it when it looks back), its
-// TMA copy then, and an L2 prefetch of the tile one CTA round further on;
-// 0: claim (and copy) at the start of this tile, a whole tile ahead
-#ifndef NDX_CLAIM_LATE
-#define NDX_CLAIM_LATE 1
-#endif
 // every lane reads its digit's counter (broadcast) instead of leader + shfl
 #ifndef NDX_WIDE_BCAST
 #define NDX_WIDE_BCAST 1
 #endif
 #ifndef NDX_AB_BCAST
 #define NDX_AB_BCAST 1  // C4 sort 2.451 vs 2.511 ms with leader read + shuffle
-#endif
-// warps that resolve the look-back of a compact-pass tile (each lane takes
-// 256 / (32 x warps) digits, their first status reads in flight together);
-// 0: every thread resolves its own digit, first read before the staging
-#ifndef NDX_AB_LB_WARPS
-#define NDX_AB_LB_WARPS 0  // 1 warp: 6.94 ms C4 sort, 2 warps: 4.51 ms, every thread: 2.50 ms
 #endif
 
 constexpr int ceil_log2(int v) { return v <= 1 ? 0 : 1 + ceil_log2((v + 1) / 2); }
@@ -102,17 +98,17 @@ struct PassShape {
   using Stage = typename std::conditional<KIND == kPassB, uint64_t, uint32_t>::type;
   static_assert(TILE <= 65536 && (TILE & (TILE - 1)) == 0, "ranks ride in 16 bits; tiles are powers of two");
   static_assert(KIND != kPassWide || LOCAL_BITS + kWideMaxBits <= 32, "wide staging packs digit | local");
-  static_assert(KIND != kPassA || LOCAL_BITS <= 16, "pass-A staging packs lo | hb | local");
+  static_assert(KIND != kPassA || LOCAL_BITS <= 16, "pass-A staging packs hb | lo | local");
 };
 
-// Shared memory of one CTA: [in: TILE u32][R: H | S][cnt NB][gbase NB][Misc]
 struct PassMisc {
   uint64_t bar;            // mbarrier of the input bulk copy
-  uint32_t tile[2];        // tile taken for iteration parity 0/1
+  uint32_t tile[2];        // pass B: tile taken for iteration parity 0/1
   uint32_t tg[2][2];       // pass B: tile_group[t], tile_group[t+1] per parity
   uint32_t sgb[2][32];     // pass B: group starts inside the tile per parity
 };
 
+// Shared memory of one CTA: [in: TILE u32][R: H | S][cnt NB][gbase NB][run NB][Misc]
 template <int KIND, int BITS>
 struct PassSmem {
   using SH = PassShape<KIND>;
@@ -125,13 +121,15 @@ struct PassSmem {
   static constexpr size_t kInOfs = 0;
   static constexpr size_t kROfs = SH::ALIAS ? 0 : kIn;
   static constexpr size_t kCntOfs = kROfs + kR;
-  static constexpr size_t kMiscOfs = kCntOfs + 2 * NB * 4;
+  static constexpr size_t kMiscOfs = kCntOfs + 3 * NB * 4;
   static constexpr size_t kBytes = kMiscOfs + sizeof(PassMisc);
 };
 
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(smem_dst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // lo16(a) | lo16(b) << 16 in one register.  Opaque to the compiler on
 // purpose: with plain shifts and ors it sees through the packing and keeps
 // the two halves in separate registers again (spilling the tile).
@@ -147,14 +145,11 @@ __device__ __forceinline__ void sts_pair(uint32_t addr, uint32_t lo, uint32_t hi
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(lo), "r"(hi) : "memory");
 }
 
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 // Everything a tile needs besides its index (one per CTA, built once).
 struct PassCtx {
   SortArgs a;
   const uint32_t* src;     // tile input (keys, or pass A's packed words)
-  const uint32_t* bstart;  // global bucket starts of this pass's digits
-  uint32_t* ctr;           // tile counter
+  const uint32_t* bstart;  // pass B: global bucket starts of its digits
   uint64_t n;
   uint32_t tiles, epoch;
   uint32_t kbase;          // wide: digit = key - kbase; A/B: the keys' top 16 bits
@@ -164,69 +159,27 @@ struct PassCtx {
   unsigned char* R;
   uint32_t* cnt;
   uint32_t* gbase;
+  uint32_t* run;           // wide/A: running global digit offsets of the chunk
   PassMisc* m;
 };
 
-template <int KIND, int BITS>
-__device__ __forceinline__ void issue_tile_copy(const PassCtx& c, uint32_t t) {  // one thread
+template <int KIND>
+__device__ __forceinline__ void issue_tile_copy(const PassCtx& c, uint64_t t) {  // one thread
   fence_proxy_async_smem();
   mbar_expect_tx(&c.m->bar, PassShape<KIND>::TILE * 4);
-  bulk_g2s(c.inbuf, c.src + uint64_t(t) * PassShape<KIND>::TILE, PassShape<KIND>::TILE * 4, &c.m->bar);
+  bulk_g2s(c.inbuf, c.src + t * PassShape<KIND>::TILE, PassShape<KIND>::TILE * 4, &c.m->bar);
 }
 
-// pass B: the groups a tile crosses, staged by cp.async a tile ahead
-__device__ __forceinline__ void group_words(const PassCtx& c, uint32_t t, int par) {  // thread 0
-  cp_async4(&c.m->tg[par][0], c.a.tile_group + t);
-  cp_async4(&c.m->tg[par][1], c.a.tile_group + t + 1);
-}
-__device__ __forceinline__ void group_starts(const PassCtx& c, int par) {  // warp 0, after tg[par] landed
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t g0 = c.m->tg[par][0], k = c.m->tg[par][1] - g0;
-  if (k <= 32 && lane < k) cp_async4(&c.m->sgb[par][lane], c.a.gb + g0 + 1 + lane);
-}
+// ---- steps shared by the three pass kinds -----------------------------------
 
-// One tile.  FULL: all TILE elements exist (every tile but the last).
-template <int KIND, int BITS>
-__device__ __forceinline__ void claim_next(const PassCtx& c, int par) {  // thread 0
-  constexpr uint32_t TILE = PassShape<KIND>::TILE;
-  const uint32_t nt = atomicAdd(c.ctr, 1u);
-  c.m->tile[par ^ 1] = nt;
-  if (nt >= c.tiles) return;
-  if (!PassShape<KIND>::ALIAS && c.bulk && uint64_t(nt + 1) * TILE <= c.n) issue_tile_copy<KIND, BITS>(c, nt);
-  if (KIND == kPassB) group_words(c, nt, par ^ 1);
-  if (NDX_CLAIM_LATE && c.bulk) {
-    const uint64_t pf = uint64_t(nt) + gridDim.x;  // about one CTA round ahead
-    if ((pf + 1) * TILE <= c.n)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c.src + pf * TILE), "r"(TILE * 4u) : "memory");
-  }
-}
-
+// 1. the tile's elements into registers (wide: digit; A: the key's low 16
+//    bits; B: the packed word)
 template <int KIND, int BITS, bool FULL>
-__device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int par, uint32_t& phase, bool later) {
-  using SH = PassShape<KIND>;
-  using Stage = typename SH::Stage;
-  constexpr uint32_t NB = 1u << BITS;
-  constexpr uint32_t DMASK = NB - 1;
-  constexpr int IPT = SH::IPT;
-  constexpr uint32_t TILE = SH::TILE;
-  constexpr uint32_t LB = SH::LOCAL_BITS;
-  constexpr bool kEarly = KIND != kPassWide && NDX_AB_LB_WARPS == 0;  // first look-back read before the staging
-  constexpr int LBW = KIND != kPassWide ? NDX_AB_LB_WARPS : 0;  // look-back warps (0: all threads)
-  const SortArgs& a = c.a;
-  uint16_t* H = reinterpret_cast<uint16_t*>(c.R);
-  Stage* S = reinterpret_cast<Stage*>(c.R);
-  uint32_t* cnt = c.cnt;
-  uint32_t* gbase = c.gbase;
-  PassMisc* m = c.m;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t ts = uint64_t(tile) * TILE;
-  const uint32_t tn = FULL ? TILE : uint32_t(c.n - ts);
-  const uint32_t wofs = uint32_t(warp) * SH::WI + lane;
-
-  // ---- 1. elements into registers
-  uint32_t x[IPT];
+__device__ __forceinline__ void load_tile(const PassCtx& c, uint64_t ts, uint32_t tn, uint32_t wofs,
+                                          uint32_t& phase, uint32_t (&x)[PassShape<KIND>::IPT]) {
+  constexpr int IPT = PassShape<KIND>::IPT;
   if (FULL && c.bulk) {
-    mbar_wait(&m->bar, phase);
+    mbar_wait(&c.m->bar, phase);
     phase ^= 1u;
 #pragma unroll
     for (int r = 0; r < IPT; ++r) x[r] = c.inbuf[wofs + r * 32];
@@ -236,31 +189,33 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
   }
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
-    if (KIND == kPassWide) x[r] = (x[r] - c.kbase) & DMASK;  // digit < 2^11; the rank goes above bit 16
-    if (KIND == kPassA) x[r] &= 0xffffu;                     // lo | hb << 8; the rank goes above bit 16
+    if (KIND == kPassWide) x[r] = (x[r] - c.kbase) & ((1u << BITS) - 1);  // the rank goes above bit 16
+    if (KIND == kPassA) x[r] &= 0xffffu;                                  // lo | hb << 8, rank above
   }
-  if (NDX_CLAIM_LATE && KIND == kPassB && later && warp == 0) {
-    // this tile's group words were requested at its claim: now its group starts
-    if (lane == 0) cp_async_wait_all();
-    __syncwarp();
-    group_starts(c, par);
-  }
-  __syncthreads();  // inbuf consumed; R free (previous scatter done)
-  if (!NDX_CLAIM_LATE && threadIdx.x == 0) claim_next<KIND, BITS>(c, par);
+}
 
-  // ---- 2. rank
+template <int KIND, int BITS>
+__device__ __forceinline__ uint32_t digit_of(uint32_t v) {
+  if (KIND == kPassB) return v >> 24;
+  return v & ((1u << BITS) - 1);
+}
+
+// 2. stable rank of every element among its warp's elements of the same
+//    digit (wide/A: into bits 16..31 of x; B: two per rk2 register); the
+//    per-warp digit counters end in H
+template <int KIND, int BITS, bool FULL>
+__device__ __forceinline__ void rank_tile(uint16_t* H, uint32_t wofs, uint32_t tn,
+                                          uint32_t (&x)[PassShape<KIND>::IPT],
+                                          uint32_t (&rk2)[PassShape<KIND>::IPT / 2]) {
+  using SH = PassShape<KIND>;
+  constexpr uint32_t NB = 1u << BITS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint16_t* Hw = H + warp * NB;
   for (uint32_t d = lane; d < NB; d += 32) Hw[d] = 0;
   __syncwarp();
-  auto digit = [&](uint32_t v) -> uint32_t {
-    if (KIND == kPassB) return v >> 24;
-    return v & DMASK;
-  };
-  constexpr bool kPackRank = KIND == kPassB;  // wide/A: the rank sits in bits 16..31 of x
-  uint32_t rk2[kPackRank ? IPT / 2 : 1];
 #pragma unroll
-  for (int r = 0; r < IPT; ++r) {
-    const uint32_t d = digit(x[r]);
+  for (int r = 0; r < SH::IPT; ++r) {
+    const uint32_t d = digit_of<KIND, BITS>(x[r]);
     unsigned peers = warp_match<BITS>(d);
     bool valid = true;
     if (!FULL) {
@@ -279,7 +234,7 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
     if (valid && lane == leader) Hw[d] = uint16_t(old + __popc(peers));
     const uint32_t rk = old + __popc(peers & lanemask_lt());
     __syncwarp();
-    if constexpr (kPackRank) {
+    if constexpr (KIND == kPassB) {
       if ((r & 1) == 0)
         rk2[r >> 1] = rk;
       else
@@ -288,38 +243,81 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
       x[r] = pack16(x[r], rk);
     }
   }
-  if (KIND == kPassB && warp == 0) cp_async_wait_all();  // this tile's group starts (issued a tile ago)
-  __syncthreads();
+}
 
-  // ---- 3. counts: warp offsets in place, tile counts published, local starts
-  uint64_t* st = a.status + uint64_t(tile) * NB;
-  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
-    uint32_t sum = 0;
+// 3a. per digit: warp offsets in place in H, the tile's count returned
+template <int KIND, int BITS>
+__device__ __forceinline__ uint32_t warp_offsets(uint16_t* H, uint32_t d) {
+  constexpr uint32_t NB = 1u << BITS;
+  uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < SH::WARPS; ++w) {
-      const uint32_t cw = H[w * NB + d];
-      H[w * NB + d] = uint16_t(sum);
-      sum += cw;
-    }
-    cnt[d] = sum;
-    st_relaxed_u64(&st[d], st_word(c.epoch, tile == 0 ? kStPrefix : kStAgg, sum));
+  for (int w = 0; w < PassShape<KIND>::WARPS; ++w) {
+    const uint32_t cw = H[w * NB + d];
+    H[w * NB + d] = uint16_t(sum);
+    sum += cw;
   }
-  __syncthreads();
-  block_excl_scan(cnt, gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+  return sum;
+}
 
-  constexpr int ND = int((NB + SH::THREADS - 1) / SH::THREADS);
-  uint64_t first[kEarly ? ND : 1] = {};
-  // global base of digit d for this tile; s0 = the status of tile-1 for d
-  // when already read (from_s0), else the look-back reads it
-  auto resolve_with = [&](uint32_t d, bool from_s0, uint64_t s0) {
-    const uint32_t cd = cnt[d], local = gbase[d];
-    uint64_t excl = 0;
-    if (tile > 0) {
-      excl = from_s0 ? lookback_from(a.status, tile, NB, d, c.epoch, s0) : lookback(a.status, tile, NB, d, c.epoch);
-      st_relaxed_u64(&st[d], st_word(c.epoch, kStPrefix, excl + cd));
-    }
-    const uint32_t gstart = c.bstart[d] + uint32_t(excl);
-    gbase[d] = gstart - local;
+// 3b. the tile-local digit start folded into every warp's offsets, then
+//     each element's rank made tile-wide
+template <int KIND, int BITS>
+__device__ __forceinline__ void add_local(uint16_t* H, uint32_t d, uint32_t local) {
+  constexpr uint32_t NB = 1u << BITS;
+#pragma unroll
+  for (int w = 0; w < PassShape<KIND>::WARPS; ++w) H[w * NB + d] += uint16_t(local);
+}
+template <int KIND, int BITS>
+__device__ __forceinline__ void rank_to_tile(const uint16_t* H, uint32_t (&x)[PassShape<KIND>::IPT],
+                                             uint32_t (&rk2)[PassShape<KIND>::IPT / 2]) {
+  constexpr uint32_t NB = 1u << BITS;
+  const uint16_t* Hw = H + (threadIdx.x >> 5) * NB;
+#pragma unroll
+  for (int r = 0; r < PassShape<KIND>::IPT; ++r) {
+    const uint32_t add = Hw[digit_of<KIND, BITS>(x[r])];
+    if constexpr (KIND == kPassB)
+      rk2[r >> 1] += add << (16 * (r & 1));
+    else
+      x[r] += add << 16;
+  }
+}
+
+// ---- wide / A: chunked, running offsets ---------------------------------------
+
+template <int KIND, int BITS, bool FULL>
+__device__ __forceinline__ void chunk_tile(const PassCtx& c, uint64_t tile, int64_t next, uint32_t& phase) {
+  using SH = PassShape<KIND>;
+  constexpr uint32_t NB = 1u << BITS;
+  constexpr uint32_t DMASK = NB - 1;
+  constexpr int IPT = SH::IPT;
+  constexpr uint32_t TILE = SH::TILE;
+  constexpr uint32_t LB = SH::LOCAL_BITS;
+  const SortArgs& a = c.a;
+  uint16_t* H = reinterpret_cast<uint16_t*>(c.R);
+  uint32_t* S = reinterpret_cast<uint32_t*>(c.R);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t ts = tile * TILE;
+  const uint32_t tn = FULL ? TILE : uint32_t(c.n - ts);
+  const uint32_t wofs = uint32_t(warp) * SH::WI + lane;
+
+  uint32_t x[IPT], rk2[IPT / 2];
+  load_tile<KIND, BITS, FULL>(c, ts, tn, wofs, phase, x);
+  __syncthreads();  // inbuf consumed; R free (previous scatter done)
+  // the next tile of this CTA's chunks is known: copy it in now
+  if (!SH::ALIAS && threadIdx.x == 0 && next >= 0 && c.bulk && uint64_t(next + 1) * TILE <= c.n)
+    issue_tile_copy<KIND>(c, uint64_t(next));
+
+  rank_tile<KIND, BITS, FULL>(H, wofs, tn, x, rk2);
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) c.cnt[d] = warp_offsets<KIND, BITS>(H, d);
+  __syncthreads();
+  block_excl_scan(c.cnt, c.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
+    const uint32_t local = c.gbase[d], cd = c.cnt[d];
+    const uint32_t gstart = c.run[d];  // where this tile's run of d begins in the output
+    c.run[d] = gstart + cd;
+    c.gbase[d] = gstart - local;
+    add_local<KIND, BITS>(H, d, local);
     if constexpr (KIND == kPassA) {
       // segment starts, and the pass-B tiles that begin inside this run
       const uint32_t seg = uint32_t(ts >> kSegBits);
@@ -327,42 +325,171 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
       for (uint32_t mt = uint32_t(ceil_div(gstart, kBTile)); uint64_t(mt) * kBTile < uint64_t(gstart) + cd; ++mt)
         a.tile_group[mt] = d * c.nseg + seg;
     }
-  };
-  auto resolve = [&](int k, uint32_t d) {
-    if constexpr (kEarly)
-      resolve_with(d, true, first[k]);
-    else
-      resolve_with(d, false, 0ull);
-    (void)k;
-  };
+  }
+  __syncthreads();
+  rank_to_tile<KIND, BITS>(H, x, rk2);
+  __syncthreads();  // H dead: S may overwrite it
+
+  // ---- staging in digit order
 #pragma unroll
-  for (int k = 0; k < ND; ++k) {
-    const uint32_t d = threadIdx.x + uint32_t(k) * SH::THREADS;
-    if (d < NB) {
-      const uint32_t local = gbase[d];
-      if constexpr (kEarly)
-        first[k] = tile > 0 ? ld_relaxed_u64(&a.status[uint64_t(tile - 1) * NB + d]) : 0ull;
-      else if constexpr (LBW == 0)
-        resolve(k, d);  // look-back first; the local starts go into the counters after it
-#pragma unroll
-      for (int w = 0; w < SH::WARPS; ++w) H[w * NB + d] += uint16_t(local);
+  for (int r = 0; r < IPT; ++r)
+    if (FULL || wofs + r * 32 < tn) {
+      const uint32_t v = x[r], local = wofs + r * 32;
+      if (KIND == kPassWide)
+        S[v >> 16] = ((v & DMASK) << LB) | local;
+      else  // hb << 24 | lo << 16 | local (v << 16 drops the rank)
+        S[v >> 16] = (v << 16) | local;
+    }
+  __syncthreads();
+
+  // ---- scatter: consecutive slots of one digit are consecutive globally
+  if constexpr (KIND == kPassA) {
+    uint32_t* out = reinterpret_cast<uint32_t*>(a.Y);
+    const uint32_t segofs = uint32_t(ts) & ((1u << kSegBits) - 1);
+#pragma unroll 4
+    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
+      const uint32_t e = S[jj];
+      out[c.gbase[(e >> 16) & 0xffu] + jj] = (e & 0xff000000u) | (segofs + (e & 0xffffu));
+    }
+  } else {
+    const uint32_t rbase = a.row_base + uint32_t(ts);
+#pragma unroll 4
+    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
+      const uint32_t e = S[jj], d = e >> LB;
+      a.X[c.gbase[d] + jj] = uint64_t(c.kbase + d) | (uint64_t(rbase + (e & ((1u << LB) - 1))) << 32);
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int r = 0; r < IPT; ++r) {
-    const uint32_t add = Hw[digit(x[r])];
-    if constexpr (kPackRank)
-      rk2[r >> 1] += add << (16 * (r & 1));
-    else
-      x[r] += add << 16;
+  if (SH::ALIAS && threadIdx.x == 0 && next >= 0 && c.bulk && uint64_t(next + 1) * TILE <= c.n)
+    issue_tile_copy<KIND>(c, uint64_t(next));
+}
+
+// The chunks of this CTA (blockIdx.x, + gridDim.x, ...), their tiles in
+// order, each chunk starting from its scanned digit offsets.
+template <int KIND, int BITS>
+__device__ __forceinline__ void run_chunked(PassCtx& c) {
+  using SH = PassShape<KIND>;
+  constexpr uint32_t NB = 1u << BITS;
+  const uint32_t K = c.a.nchunk;
+  auto first_tile = [&](uint32_t ch) -> int64_t {
+    if (ch >= K) return -1;
+    const uint64_t e0 = chunk_begin(c.n, K, ch), e1 = chunk_begin(c.n, K, ch + 1);
+    return e1 > e0 ? int64_t(e0 / SH::TILE) : -1;
+  };
+  uint32_t ch = blockIdx.x;
+  while (ch < K && first_tile(ch) < 0) ch += gridDim.x;
+  if (ch >= K) return;
+  if (threadIdx.x == 0) {
+    mbar_init(&c.m->bar, 1);
+    fence_mbar_init();
+    const int64_t t = first_tile(ch);
+    if (c.bulk && uint64_t(t + 1) * SH::TILE <= c.n) issue_tile_copy<KIND>(c, uint64_t(t));
   }
+  __syncthreads();
+  uint32_t phase = 0;
+  while (ch < K) {
+    const uint64_t t0 = chunk_begin(c.n, K, ch) / SH::TILE;
+    const uint64_t t1 = ceil_div(chunk_begin(c.n, K, ch + 1), SH::TILE);
+    uint32_t nch = ch + gridDim.x;
+    while (nch < K && first_tile(nch) < 0) nch += gridDim.x;
+    const uint32_t* off = c.a.chunk_off + uint64_t(ch) * kWideBuckets;
+    for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) c.run[d] = off[d];
+    // (visible after the first barrier of the chunk's first tile)
+    for (uint64_t t = t0; t < t1; ++t) {
+      const int64_t next = t + 1 < t1 ? int64_t(t + 1) : first_tile(nch);
+      if ((t + 1) * SH::TILE <= c.n)
+        chunk_tile<KIND, BITS, true>(c, t, next, phase);
+      else
+        chunk_tile<KIND, BITS, false>(c, t, next, phase);
+    }
+    ch = nch;
+  }
+}
+
+// ---- B: look-back ---------------------------------------------------------------
+
+// pass B: the groups a tile crosses, staged by cp.async
+__device__ __forceinline__ void group_words(const PassCtx& c, uint32_t t, int par) {  // thread 0
+  cp_async4(&c.m->tg[par][0], c.a.tile_group + t);
+  cp_async4(&c.m->tg[par][1], c.a.tile_group + t + 1);
+}
+__device__ __forceinline__ void group_starts(const PassCtx& c, int par) {  // warp 0, after tg[par] landed
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t g0 = c.m->tg[par][0], k = c.m->tg[par][1] - g0;
+  if (k <= 32 && lane < k) cp_async4(&c.m->sgb[par][lane], c.a.gb + g0 + 1 + lane);
+}
+
+// Takes the next tile at the end of this one (claim order == processing
+// order, so a tile's predecessors are ahead of it when it looks back),
+// copies it in, requests its group words, and prefetches the tile one CTA
+// round further on into L2.
+__device__ __forceinline__ void claim_next_b(const PassCtx& c, uint32_t* ctr, int par) {  // thread 0
+  using SH = PassShape<kPassB>;
+  const uint32_t nt = atomicAdd(ctr, 1u);
+  c.m->tile[par ^ 1] = nt;
+  if (nt >= c.tiles) return;
+  if (!SH::ALIAS && uint64_t(nt + 1) * SH::TILE <= c.n) issue_tile_copy<kPassB>(c, nt);
+  group_words(c, nt, par ^ 1);
+  const uint64_t pf = uint64_t(nt) + gridDim.x;
+  if ((pf + 1) * SH::TILE <= c.n)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c.src + pf * SH::TILE), "r"(SH::TILE * 4u)
+                 : "memory");
+}
+
+template <bool FULL>
+__device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, uint32_t tile, int par,
+                                              uint32_t& phase, bool later) {
+  constexpr int KIND = kPassB;
+  constexpr int BITS = 8;
+  using SH = PassShape<KIND>;
+  constexpr uint32_t NB = 256;
+  constexpr int IPT = SH::IPT;
+  constexpr uint32_t TILE = SH::TILE;
+  const SortArgs& a = c.a;
+  uint16_t* H = reinterpret_cast<uint16_t*>(c.R);
+  uint64_t* S = reinterpret_cast<uint64_t*>(c.R);
+  PassMisc* m = c.m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t ts = uint64_t(tile) * TILE;
+  const uint32_t tn = FULL ? TILE : uint32_t(c.n - ts);
+  const uint32_t wofs = uint32_t(warp) * SH::WI + lane;
+
+  uint32_t x[IPT], rk2[IPT / 2];
+  load_tile<KIND, BITS, FULL>(c, ts, tn, wofs, phase, x);
+  if (later && warp == 0) {
+    // this tile's group words were requested at its claim: now its group starts
+    if (lane == 0) cp_async_wait_all();
+    __syncwarp();
+    group_starts(c, par);
+  }
+  __syncthreads();  // inbuf consumed; R free (previous scatter done)
+
+  rank_tile<KIND, BITS, FULL>(H, wofs, tn, x, rk2);
+  if (warp == 0) cp_async_wait_all();  // this tile's group starts
+  __syncthreads();
+
+  // counts published (decoupled look-back status), local starts
+  uint64_t* st = a.status + uint64_t(tile) * NB;
+  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
+    const uint32_t sum = warp_offsets<KIND, BITS>(H, d);
+    c.cnt[d] = sum;
+    st_relaxed_u64(&st[d], st_word(c.epoch, tile == 0 ? kStPrefix : kStAgg, sum));
+  }
+  __syncthreads();
+  block_excl_scan(c.cnt, c.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+  // the first predecessor status of this thread's digit is requested now;
+  // its round trip overlaps the rank adjustment and the staging
+  static_assert(SH::THREADS == int(NB), "one digit per thread");
+  const uint32_t dme = threadIdx.x;
+  const uint64_t first = tile > 0 ? ld_relaxed_u64(&a.status[uint64_t(tile - 1) * NB + dme]) : 0ull;
+  add_local<KIND, BITS>(H, dme, c.gbase[dme]);
+  __syncthreads();
+  rank_to_tile<KIND, BITS>(H, x, rk2);
   __syncthreads();  // H dead: S may overwrite it
 
-  // ---- 4. staging in digit order
-  if constexpr (KIND == kPassB) {
-    // group (lo, seg) of each element: walk the group starts inside the
-    // tile (positions increase with r)
+  // ---- staging: the final (key, row) pair.  The group (lo, seg) of each
+  // element: walk the group starts inside the tile (positions grow with r)
+  {
     const uint32_t g0 = m->tg[par][0], k = m->tg[par][1] - g0;
     const uint32_t* sg = m->sgb[par];
     const uint32_t p0 = uint32_t(ts) + wofs;
@@ -387,106 +514,96 @@ __device__ __forceinline__ void tma_tile(const PassCtx& c, uint32_t tile, int pa
         }
     } else {
 #pragma unroll
-    for (int r = 0; r < IPT; ++r) {
-      const uint32_t p = p0 + uint32_t(r) * 32;
-      if (k <= 32) {
-        if (p >= nb) {
-          while (j < k && p >= sg[j]) ++j;
-          nb = j < k ? sg[j] : 0xffffffffu;
-          set_group(g0 + j);
+      for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = p0 + uint32_t(r) * 32;
+        if (k <= 32) {
+          if (p >= nb) {
+            while (j < k && p >= sg[j]) ++j;
+            nb = j < k ? sg[j] : 0xffffffffu;
+            set_group(g0 + j);
+          }
+        } else {
+          // pathological tile (more than 32 groups start inside it): count
+          // the group starts GB[g0+1 .. g0+k] <= p by binary search
+          uint32_t lo_i = 0, hi_i = k;
+          while (lo_i < hi_i) {
+            const uint32_t mid = (lo_i + hi_i) >> 1;
+            if (__ldg(a.gb + g0 + 1 + mid) <= p)
+              lo_i = mid + 1;
+            else
+              hi_i = mid;
+          }
+          set_group(g0 + lo_i);
         }
-      } else {
-        // pathological tile (more than 32 groups start inside it): count the
-        // group starts GB[g0+1 .. g0+k] <= p by binary search
-        uint32_t lo_i = 0, hi_i = k;
-        while (lo_i < hi_i) {
-          const uint32_t mid = (lo_i + hi_i) >> 1;
-          if (__ldg(a.gb + g0 + 1 + mid) <= p)
-            lo_i = mid + 1;
-          else
-            hi_i = mid;
+        if (FULL || wofs + r * 32 < tn) {
+          const uint32_t v = x[r];
+          sts_pair(s_base + 8u * ((rk2[r >> 1] >> (16 * (r & 1))) & 0xffffu), kb | ((v >> 24) << 8),
+                   rb + (v & 0xffffffu));
         }
-        set_group(g0 + lo_i);
-      }
-      if (FULL || wofs + r * 32 < tn) {
-        const uint32_t v = x[r];
-        sts_pair(s_base + 8u * ((rk2[r >> 1] >> (16 * (r & 1))) & 0xffffu), kb | ((v >> 24) << 8),
-                 rb + (v & 0xffffffu));
       }
     }
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < IPT; ++r)
-      if (FULL || wofs + r * 32 < tn) {
-        const uint32_t v = x[r], local = wofs + r * 32;
-        if (KIND == kPassWide)
-          S[v >> 16] = ((v & DMASK) << LB) | local;
-        else  // hb << 24 | lo << 16 | local (v << 16 drops the rank)
-          S[v >> 16] = (v << 16) | local;
-      }
   }
-  if constexpr (kEarly) {
-    // look-back, part 2: finish from the status already in hand
-#pragma unroll
-    for (int k = 0; k < ND; ++k) {
-      const uint32_t d = threadIdx.x + uint32_t(k) * SH::THREADS;
-      if (d < NB) resolve(k, d);
+
+  // ---- look-back: this tile's global base for my digit
+  {
+    const uint32_t cd = c.cnt[dme], local = c.gbase[dme];
+    uint64_t excl = 0;
+    if (tile > 0) {
+      excl = lookback_from(a.status, tile, NB, dme, c.epoch, first);
+      st_relaxed_u64(&st[dme], st_word(c.epoch, kStPrefix, excl + cd));
     }
-  } else if constexpr (LBW > 0) {
-    // LBW warps resolve every digit: the first status of each of a lane's
-    // digits is requested at once, the rest of the CTA does not spin
-    if (warp < LBW) {
-      constexpr int DPL = int(NB) / (32 * LBW);
-      static_assert(DPL * 32 * LBW == int(NB), "digits per look-back lane");
-      uint64_t s0[DPL];
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) {
-        const uint32_t d = uint32_t(lane + 32 * (warp + LBW * j));
-        s0[j] = tile > 0 ? ld_relaxed_u64(&a.status[uint64_t(tile - 1) * NB + d]) : 0ull;
-      }
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) resolve_with(uint32_t(lane + 32 * (warp + LBW * j)), true, s0[j]);
-    }
+    c.gbase[dme] = c.bstart[dme] + uint32_t(excl) - local;
   }
   __syncthreads();
 
-  // ---- 5. scatter: consecutive slots of one digit are consecutive globally
-  if constexpr (KIND == kPassA) {
-    uint32_t* out = reinterpret_cast<uint32_t*>(a.Y);
-    const uint32_t segofs = uint32_t(ts) & ((1u << kSegBits) - 1);
+  // ---- scatter
 #pragma unroll 4
-    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
-      const uint32_t e = S[jj];
-      out[gbase[(e >> 16) & 0xffu] + jj] = (e & 0xff000000u) | (segofs + (e & 0xffffu));
-    }
-  } else if constexpr (KIND == kPassWide) {
-    const uint32_t rbase = a.row_base + uint32_t(ts);
-#pragma unroll 4
-    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
-      const uint32_t e = S[jj], d = e >> LB;
-      a.X[gbase[d] + jj] = uint64_t(c.kbase + d) | (uint64_t(rbase + (e & ((1u << LB) - 1))) << 32);
-    }
-  } else {
-#pragma unroll 4
-    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
-      const uint64_t e = S[jj];
-      a.X[gbase[(uint32_t(e) >> 8) & 0xffu] + jj] = e;
-    }
+  for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
+    const uint64_t e = S[jj];
+    a.X[c.gbase[(uint32_t(e) >> 8) & 0xffu] + jj] = e;
   }
-  if (NDX_CLAIM_LATE) {
-    if (threadIdx.x == 0) claim_next<KIND, BITS>(c, par);
-  } else if (KIND == kPassB && warp == 0 && m->tile[par ^ 1] < c.tiles) {
-    if (lane == 0) cp_async_wait_all();  // tile_group words of the next tile
-    __syncwarp();
-    group_starts(c, par ^ 1);
-  }
+  if (threadIdx.x == 0) claim_next_b(c, ctr, par);
   __syncthreads();
   if (SH::ALIAS && threadIdx.x == 0) {
     const uint32_t nt = m->tile[par ^ 1];
-    if (nt < c.tiles && c.bulk && uint64_t(nt + 1) * TILE <= c.n) issue_tile_copy<KIND, BITS>(c, nt);
+    if (nt < c.tiles && uint64_t(nt + 1) * TILE <= c.n) issue_tile_copy<KIND>(c, nt);
   }
 }
+
+__device__ __forceinline__ void run_lookback_b(PassCtx& c) {
+  using SH = PassShape<kPassB>;
+  uint32_t* ctr = &c.a.ctl->tile_ctr[kCtrB];
+  PassMisc* m = c.m;
+  if (threadIdx.x == 0) {
+    mbar_init(&m->bar, 1);
+    fence_mbar_init();
+    const uint32_t t = atomicAdd(ctr, 1u);
+    m->tile[0] = t;
+    if (t < c.tiles && uint64_t(t + 1) * SH::TILE <= c.n) issue_tile_copy<kPassB>(c, t);
+    if (t < c.tiles) {
+      group_words(c, t, 0);
+      cp_async_wait_all();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && m->tile[0] < c.tiles) {
+    group_starts(c, 0);
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int it = 0;; ++it) {
+    const int par = it & 1;
+    const uint32_t tile = m->tile[par];
+    if (tile >= c.tiles) break;
+    if (uint64_t(tile + 1) * SH::TILE <= c.n)
+      lookback_tile<true>(c, ctr, tile, par, phase, it > 0);
+    else
+      lookback_tile<false>(c, ctr, tile, par, phase, it > 0);
+  }
+}
+
+// ---- kernels ------------------------------------------------------------------
 
 // digit width class of the wide pass (the instantiation that runs it)
 __host__ __device__ inline int wide_class(uint32_t bits) { return bits <= 4 ? 4 : bits <= 8 ? 8 : bits <= 9 ? 9 : bits <= 10 ? 10 : 11; }
@@ -501,47 +618,21 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, int bulk_ok, unsigne
   c.R = smem + SM::kROfs;
   c.cnt = reinterpret_cast<uint32_t*>(smem + SM::kCntOfs);
   c.gbase = c.cnt + SM::NB;
+  c.run = c.gbase + SM::NB;
   c.m = reinterpret_cast<PassMisc*>(smem + SM::kMiscOfs);
   const SortPlan& pl = a.ctl->plan;
   c.n = a.n;
   c.tiles = uint32_t(ceil_div(a.n, SH::TILE));
-  c.ctr = &a.ctl->tile_ctr[KIND == kPassWide ? kCtrWide : (KIND == kPassA ? kCtrA : kCtrB)];
-  c.epoch = a.ctl->epoch + (KIND == kPassWide ? kEpochWide : (KIND == kPassA ? kEpochA : kEpochB));
+  c.epoch = a.ctl->epoch + kEpochB;
   c.src = KIND == kPassB ? reinterpret_cast<const uint32_t*>(a.Y) : a.in_keys;
-  c.bstart = KIND == kPassWide ? pl.bucket_start_wide : (KIND == kPassA ? pl.bucket_start_byte[0] : pl.bucket_start_byte[1]);
+  c.bstart = pl.bucket_start_byte[1];
   c.kbase = pl.base;
   c.nseg = pl.nseg;
   c.bulk = bulk_ok != 0;
-  PassMisc* m = c.m;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&m->bar, 1);
-    fence_mbar_init();
-    const uint32_t t = atomicAdd(c.ctr, 1u);
-    m->tile[0] = t;
-    if (t < c.tiles && c.bulk && uint64_t(t + 1) * SH::TILE <= c.n) issue_tile_copy<KIND, BITS>(c, t);
-    if (KIND == kPassB && t < c.tiles) {
-      group_words(c, t, 0);
-      cp_async_wait_all();
-    }
-  }
-  __syncthreads();
-  if (KIND == kPassB && threadIdx.x < 32 && m->tile[0] < c.tiles) {
-    group_starts(c, 0);
-    cp_async_wait_all();
-  }
-  __syncthreads();
-
-  uint32_t phase = 0;
-  for (int it = 0;; ++it) {
-    const int par = it & 1;
-    const uint32_t tile = m->tile[par];
-    if (tile >= c.tiles) break;
-    if (uint64_t(tile + 1) * SH::TILE <= c.n)
-      tma_tile<KIND, BITS, true>(c, tile, par, phase, it > 0);
-    else
-      tma_tile<KIND, BITS, false>(c, tile, par, phase, it > 0);
-  }
+  if constexpr (KIND == kPassB)
+    run_lookback_b(c);
+  else
+    run_chunked<KIND, BITS>(c);
 }
 
 // One kernel per pass kind; the wide pass picks its digit width at run
@@ -595,12 +686,33 @@ static int pass_attr(int* occ) {
   return e;
 }
 
-static int pass_cfg_init(PassCfg& c, int dev) {
-  int e;
-  if ((e = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-  if ((e = pass_attr<kPassWide>(&c.occ_wide))) return e;
-  if ((e = pass_attr<kPassA>(&c.occ_a))) return e;
-  if ((e = pass_attr<kPassB>(&c.occ_b))) return e;
+static int pass_cfg(const PassCfg** out) {
+  static PassCfg cfg[64];
+  static std::once_flag once[64];
+  static int rc_of[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  std::call_once(once[dev & 63], [dev] {
+    PassCfg& c = cfg[dev & 63];
+    int& rc = rc_of[dev & 63];
+    if ((rc = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev))) return;
+    if ((rc = pass_attr<kPassWide>(&c.occ_wide))) return;
+    if ((rc = pass_attr<kPassA>(&c.occ_a))) return;
+    rc = pass_attr<kPassB>(&c.occ_b);
+  });
+  if (rc_of[dev & 63]) return rc_of[dev & 63];
+  *out = &cfg[dev & 63];
+  return 0;
+}
+
+// The first pass's chunk count for n keys on this device: one chunk per
+// resident pass-A CTA (the wide pass walks several per CTA).
+int first_pass_chunks(uint64_t n, uint32_t* k) {
+  const PassCfg* c;
+  int rc = pass_cfg(&c);
+  if (rc) return rc;
+  *k = chunk_count(n, uint32_t(c->sms * c->occ_a));
   return 0;
 }
 
@@ -610,28 +722,22 @@ static int pass_cfg_init(PassCfg& c, int dev) {
 // ms slower on C4: device-launched grids of the compact passes ran at about
 // two thirds of their host-launched speed; ncu does not profile them either.)
 int launch_sort_dispatch(const SortArgs& a, int legacy, int byte_grid, int legacy_wide_grid, cudaStream_t s) {
-  static PassCfg cfg[64];
-  static std::once_flag once[64];
-  static int rc_of[64];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e) return e;
-  std::call_once(once[dev & 63], [dev] { rc_of[dev & 63] = pass_cfg_init(cfg[dev & 63], dev); });
-  if (rc_of[dev & 63]) return rc_of[dev & 63];
-  const PassCfg& c = cfg[dev & 63];
+  const PassCfg* c;
+  int rc = pass_cfg(&c);
+  if (rc) return rc;
   const int bulk_keys = (reinterpret_cast<uintptr_t>(a.in_keys) & 15u) == 0;
   k_set_row_hi<<<1, 1, 0, s>>>(a);
   if (legacy) {
     k_pass<kWideMaxBits, 0><<<legacy_wide_grid, 512, kLegacyWideSmem, s>>>(a, -1);
   } else {
-    const int gw = int(umin<uint64_t>(ceil_div(a.n, kWideTile), uint64_t(c.sms) * c.occ_wide));
-    const int ga = int(umin<uint64_t>(ceil_div(a.n, kATile), uint64_t(c.sms) * c.occ_a));
-    const int gb = int(umin<uint64_t>(ceil_div(a.n, kBTile), uint64_t(c.sms) * c.occ_b));
+    const int gw = int(umin<uint64_t>(a.nchunk, uint64_t(c->sms) * c->occ_wide));
+    const int gb = int(umin<uint64_t>(ceil_div(a.n, kBTile), uint64_t(c->sms) * c->occ_b));
     k_tma_pass<kPassWide><<<gw, PassShape<kPassWide>::THREADS, pass_smem<kPassWide>(), s>>>(a, bulk_keys);
-    k_tma_pass<kPassA><<<ga, PassShape<kPassA>::THREADS, pass_smem<kPassA>(), s>>>(a, bulk_keys);
+    k_tma_pass<kPassA><<<a.nchunk, PassShape<kPassA>::THREADS, pass_smem<kPassA>(), s>>>(a, bulk_keys);
     k_tma_pass<kPassB><<<gb, PassShape<kPassB>::THREADS, pass_smem<kPassB>(), s>>>(a, 1);
   }
-  if ((e = cudaGetLastError())) return e;
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
   // general keys: every byte pass in one cooperative launch (grid barriers)
   SortArgs args = a;
   void* params[] = {&args};

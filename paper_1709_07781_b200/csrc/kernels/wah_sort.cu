@@ -67,16 +67,17 @@ static_assert(Shape<8>::TILE == kLegacyByteTile && Shape<kWideMaxBits>::TILE == 
 constexpr int kHistThreads = 512;
 
 // Key range, low-11-bit histogram and byte-1 histogram in one read of the
-// keys.  The byte-0 histogram is the low-11 one folded (2 shared atomics per
-// key, not 3), and every group of four warps counts into its own copy so a
-// skewed column's hot bins are not one shared-memory hot spot.
+// keys, counted per chunk of the first pass (chunk_begin): each CTA takes
+// whole chunks, writes every chunk's 11-bit counts (the plan scans them into
+// the first pass's per-chunk offsets) and adds them to the column's.  Every
+// group of four warps counts into its own copy so a skewed column's hot bins
+// are not one shared-memory hot spot.
 constexpr int kHistCopies = 4;
 __global__ __launch_bounds__(kHistThreads, 1) void k_hist(const uint32_t* __restrict__ keys, uint64_t n,
-                                                          Ctl* ctl) {
+                                                          Ctl* ctl, uint32_t* __restrict__ chunk_hist,
+                                                          uint32_t nchunk) {
   __shared__ uint32_t hws[kHistCopies][kWideBuckets], h1s[kHistCopies][256];
-  for (int i = threadIdx.x; i < kHistCopies * kWideBuckets; i += blockDim.x) (&hws[0][0])[i] = 0;
   for (int i = threadIdx.x; i < kHistCopies * 256; i += blockDim.x) (&h1s[0][0])[i] = 0;
-  __syncthreads();
   const int copy = (threadIdx.x >> 5) & (kHistCopies - 1);
   uint32_t* hw = hws[copy];
   uint32_t* h1 = h1s[copy];
@@ -87,42 +88,57 @@ __global__ __launch_bounds__(kHistThreads, 1) void k_hist(const uint32_t* __rest
     atomicAdd(&hw[k & (kWideBuckets - 1)], 1u);
     atomicAdd(&h1[(k >> 8) & 255u], 1u);
   };
-  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  if ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0) {
-    const uint4* q = reinterpret_cast<const uint4*>(keys);
-    const uint64_t nq = n / 4;
-    uint64_t i = tid;
-    // 4 loads in flight, and the next 4 issued before this batch's atomics
-    if (i + 3 * stride < nq) {
-      uint4 v0 = ldg_stream4(q + i), v1 = ldg_stream4(q + i + stride);
-      uint4 v2 = ldg_stream4(q + i + 2 * stride), v3 = ldg_stream4(q + i + 3 * stride);
-      for (;;) {
-        const uint64_t nx = i + 4 * stride;
-        const bool more = nx + 3 * stride < nq;
-        uint4 w0 = v0, w1 = v1, w2 = v2, w3 = v3;
-        if (more) {
-          w0 = ldg_stream4(q + nx);
-          w1 = ldg_stream4(q + nx + stride);
-          w2 = ldg_stream4(q + nx + 2 * stride);
-          w3 = ldg_stream4(q + nx + 3 * stride);
+  const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15u) == 0;  // chunk bounds are 16-key multiples
+  for (uint32_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
+    for (int i = threadIdx.x; i < kHistCopies * kWideBuckets; i += blockDim.x) (&hws[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t e0 = chunk_begin(n, nchunk, c), e1 = chunk_begin(n, nchunk, c + 1);
+    if (vec) {
+      const uint4* q = reinterpret_cast<const uint4*>(keys + e0);
+      const uint64_t nq = (e1 - e0) / 4;
+      const uint64_t stride = blockDim.x;
+      uint64_t i = threadIdx.x;
+      // 4 loads in flight, and the next 4 issued before this batch's atomics
+      if (i + 3 * stride < nq) {
+        uint4 v0 = ldg_stream4(q + i), v1 = ldg_stream4(q + i + stride);
+        uint4 v2 = ldg_stream4(q + i + 2 * stride), v3 = ldg_stream4(q + i + 3 * stride);
+        for (;;) {
+          const uint64_t nx = i + 4 * stride;
+          const bool more = nx + 3 * stride < nq;
+          uint4 w0 = v0, w1 = v1, w2 = v2, w3 = v3;
+          if (more) {
+            w0 = ldg_stream4(q + nx);
+            w1 = ldg_stream4(q + nx + stride);
+            w2 = ldg_stream4(q + nx + 2 * stride);
+            w3 = ldg_stream4(q + nx + 3 * stride);
+          }
+          one(v0.x); one(v0.y); one(v0.z); one(v0.w);
+          one(v1.x); one(v1.y); one(v1.z); one(v1.w);
+          one(v2.x); one(v2.y); one(v2.z); one(v2.w);
+          one(v3.x); one(v3.y); one(v3.z); one(v3.w);
+          i = nx;
+          if (!more) break;
+          v0 = w0; v1 = w1; v2 = w2; v3 = w3;
         }
-        one(v0.x); one(v0.y); one(v0.z); one(v0.w);
-        one(v1.x); one(v1.y); one(v1.z); one(v1.w);
-        one(v2.x); one(v2.y); one(v2.z); one(v2.w);
-        one(v3.x); one(v3.y); one(v3.z); one(v3.w);
-        i = nx;
-        if (!more) break;
-        v0 = w0; v1 = w1; v2 = w2; v3 = w3;
       }
+      for (; i < nq; i += stride) {
+        const uint4 v = ldg_stream4(q + i);
+        one(v.x); one(v.y); one(v.z); one(v.w);
+      }
+      for (uint64_t j = e0 + nq * 4 + threadIdx.x; j < e1; j += stride) one(keys[j]);
+    } else {
+      for (uint64_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) one(keys[j]);
     }
-    for (; i < nq; i += stride) {
-      const uint4 v = ldg_stream4(q + i);
-      one(v.x); one(v.y); one(v.z); one(v.w);
+    __syncthreads();
+    uint32_t* out = chunk_hist + uint64_t(c) * kWideBuckets;
+    for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x) {
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < kHistCopies; ++k) cnt += hws[k][i];
+      out[i] = cnt;
+      if (cnt) atomicAdd(&ctl->hist_wide[i], cnt);
     }
-    for (uint64_t j = nq * 4 + tid; j < n; j += stride) one(keys[j]);
-  } else {
-    for (uint64_t j = tid; j < n; j += stride) one(keys[j]);
+    __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -133,26 +149,11 @@ __global__ __launch_bounds__(kHistThreads, 1) void k_hist(const uint32_t* __rest
     atomicMax(&ctl->max_seen, mx);
     atomicMax(&ctl->max_not, mxn);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int k = 0; k < kHistCopies; ++k) c += hws[k][i];
-    hws[0][i] = c;
-    if (c) atomicAdd(&ctl->hist_wide[i], c);
-  }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    uint32_t c = 0;
+    uint32_t cnt = 0;
 #pragma unroll
-    for (int k = 0; k < kHistCopies; ++k) c += h1s[k][i];
-    if (c) atomicAdd(&ctl->hist_byte[1][i], c);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < kWideBuckets / 256; ++j) c += hws[0][i + 256 * j];
-    if (c) atomicAdd(&ctl->hist_byte[0][i], c);
+    for (int k = 0; k < kHistCopies; ++k) cnt += h1s[k][i];
+    if (cnt) atomicAdd(&ctl->hist_byte[1][i], cnt);
   }
 }
 
@@ -223,6 +224,13 @@ __global__ __launch_bounds__(1024) void k_plan(PlanArgs a, int stage) {
   __shared__ uint32_t s_mode, s_wrap, s_hi;
   __shared__ uint32_t rot[kWideBuckets];
   const uint32_t mn = ~ctl->max_not, mx = ctl->max_seen;
+  // byte 0's histogram is the low-11-bit one folded
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = 0;
+    for (int j = 0; j < kWideBuckets / 256; ++j) c += ctl->hist_wide[i + 256 * j];
+    ctl->hist_byte[0][i] = c;
+  }
+  __syncthreads();
   // The tags are 24 bits: after 2^21 builds they come round again, and a
   // status left by a build one cycle ago (at tiles no build since has
   // reached) would read as ready.  So on the wrap every status ever written
@@ -280,6 +288,62 @@ __global__ __launch_bounds__(1024) void k_plan(PlanArgs a, int stage) {
   } else if (threadIdx.x == 0) {
     k_hist_hi<<<a.hist_hi_grid, kHistThreads, 0, cudaStreamTailLaunch>>>(a.keys, n, ctl);
     k_plan<<<1, 1024, 0, cudaStreamTailLaunch>>>(a, 1);
+  }
+}
+
+// Per-chunk digit offsets of the first pass (wide or A): chunk c's run of
+// digit d starts at bucket_start[d] + the count of d in chunks < c.  One CTA
+// per 32 digits: warp g sums its slice of the chunks for every digit (lane),
+// the slices are scanned, then each warp writes its chunks' offsets.
+__global__ __launch_bounds__(1024) void k_chunk_scan(const Ctl* ctl, const uint32_t* __restrict__ chunk_hist,
+                                                     uint32_t* __restrict__ chunk_off, uint32_t nchunk) {
+  const SortPlan& p = ctl->plan;
+  const uint32_t mode = p.mode;
+  uint32_t nb;
+  const uint32_t* bstart;
+  if (mode == kModeWide) {
+    nb = 1u << p.wide_bits;
+    bstart = p.bucket_start_wide;
+  } else if (mode == kModeAB) {
+    nb = 256;
+    bstart = p.bucket_start_byte[0];
+  } else {
+    return;
+  }
+  if (blockIdx.x * 32 >= nb) return;
+  __shared__ uint32_t part[32][33];
+  const uint32_t lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const uint32_t d = blockIdx.x * 32 + lane;
+  const uint32_t mn = ctl->min_key;
+  auto count = [&](uint32_t c) -> uint32_t {
+    const uint32_t* h = chunk_hist + uint64_t(c) * kWideBuckets;
+    if (mode == kModeWide) return __ldg(h + ((d + mn) & (kWideBuckets - 1)));
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kWideBuckets / 256; ++j) s += __ldg(h + d + 256 * j);  // byte 0: the 11 bits folded
+    return s;
+  };
+  const uint32_t c0 = uint32_t(uint64_t(nchunk) * g / 32), c1 = uint32_t(uint64_t(nchunk) * (g + 1) / 32);
+  uint32_t sum = 0;
+  if (d < nb)
+    for (uint32_t c = c0; c < c1; ++c) sum += count(c);
+  part[g][lane] = sum;
+  __syncthreads();
+  if (g == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t t = part[k][lane];
+      part[k][lane] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  if (d < nb) {
+    uint32_t run = bstart[d] + part[g][lane];
+    for (uint32_t c = c0; c < c1; ++c) {
+      chunk_off[uint64_t(c) * kWideBuckets + d] = run;
+      run += count(c);
+    }
   }
 }
 
@@ -653,6 +717,8 @@ __global__ __launch_bounds__(Shape<8>::THREADS, Shape<8>::MINB) void k_pass_byte
 
 // ------------------------------------------------------------------ host --
 
+int first_pass_chunks(uint64_t n, uint32_t* k);  // wah_pass.cu
+
 struct LegacyCfg {
   int sms = 0;
   int occ_wide = 1, occ_byte = 1, occ_hist = 1;
@@ -696,9 +762,12 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, char* status_
   if (rc) return rc;
   cudaError_t e = cudaMemsetAsync(ctl, 0, offsetof(Ctl, zero_end), s);
   if (e) return e;
+  uint32_t nchunk = 0;
+  if ((rc = first_pass_chunks(n, &nchunk))) return rc;
+  uint32_t* chunk_hist = reinterpret_cast<uint32_t*>(status_buf + kChunkHistOffset);
   // one wave: every CTA resident (a second partial wave would run alone)
-  const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * c->occ_hist, ceil_div(n, 65536))));
-  k_hist<<<grid, kHistThreads, 0, s>>>(keys, n, ctl);
+  const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * c->occ_hist, nchunk)));
+  k_hist<<<grid, kHistThreads, 0, s>>>(keys, n, ctl, chunk_hist, nchunk);
   PlanArgs pa;
   pa.keys = keys;
   pa.n = n;
@@ -708,6 +777,8 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, char* status_
   pa.allow_compact = allow_compact;
   pa.hist_hi_grid = c->sms * 2;
   k_plan<<<1, 1024, 0, s>>>(pa, 0);
+  k_chunk_scan<<<kWideBuckets / 32, 1024, 0, s>>>(ctl, chunk_hist,
+                                                   reinterpret_cast<uint32_t*>(status_buf + kChunkOffOffset), nchunk);
   return cudaGetLastError();
 }
 
@@ -715,6 +786,8 @@ static SortArgs sort_args(uint64_t n, Ctl* ctl, char* status_buf) {
   SortArgs a{};
   a.n = n;
   a.ctl = ctl;
+  a.chunk_off = reinterpret_cast<const uint32_t*>(status_buf + kChunkOffOffset);
+  first_pass_chunks(n, &a.nchunk);
   a.status = reinterpret_cast<uint64_t*>(status_buf + kStatusOffset);
   a.gb = reinterpret_cast<uint32_t*>(status_buf + kGbOffset);
   a.tile_group = reinterpret_cast<uint32_t*>(status_buf + kTgOffset);

@@ -145,20 +145,48 @@ constexpr int kBTile = NDX_AB_THREADS * NDX_B_IPT;
 constexpr int kSegBits = 24;
 static_assert((1 << kSegBits) % kATile == 0, "a pass-A tile never straddles a row segment");
 
+// ---- chunks of the first pass ------------------------------------------
+// The first pass (wide or A) reads the keys in their original order, so its
+// digit counts per stretch of keys are known before it runs: the plan stage
+// counts each chunk (a contiguous range of whole kChunkBlock-key blocks),
+// scans the counts into per-chunk digit offsets, and the pass walks its
+// chunks in order with running offsets -- no look-back, no waiting.
+constexpr uint64_t kChunkBlock = 16384;
+constexpr uint32_t kMaxChunks = 512;
+static_assert(kChunkBlock % kWideTile == 0 && kChunkBlock % kATile == 0, "tiles nest in chunk blocks");
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+// [first, last) element of chunk c of k over n keys
+__host__ __device__ inline uint64_t chunk_begin(uint64_t n, uint32_t k, uint32_t c) {
+  const uint64_t blocks = ceil_div(n, kChunkBlock);
+  const uint64_t b = blocks * c / k;
+  return b * kChunkBlock < n ? b * kChunkBlock : n;
+}
+// the chunk count for n keys: `want` (the first pass's CTA count), at most
+// one per block and kMaxChunks
+__host__ __device__ inline uint32_t chunk_count(uint64_t n, uint32_t want) {
+  const uint64_t blocks = ceil_div(n, kChunkBlock);
+  uint64_t k = want < blocks ? want : blocks;
+  k = k < kMaxChunks ? k : kMaxChunks;
+  return uint32_t(k < 1 ? 1 : k);
+}
+
 // ---- status buffer layout ----------------------------------------------
 // Fixed offsets, independent of n (a region never holds another region's
 // data from an earlier build of a different size):
 // [256 B header: u32 epoch counter, u32 pad, u64 high-water mark]
 // [GB: segment starts of the compact mode, 256 x kMaxSeg u32]
 // [tile_group: pass-B tile -> group of its first element, kMaxTilesB + 1 u32]
+// [chunk counts: kMaxChunks x 2048 u32 (low 11 bits of the key)]
+// [chunk offsets: kMaxChunks x 2048 u32 (first-pass digit)]
 // [statuses: the pass with the most (tiles x digits), u64 each]
-__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 constexpr uint64_t kMaxValues = 1ull << 31;  // a build takes n < 2^31
 constexpr uint64_t kMaxSeg = kMaxValues >> kSegBits;
 constexpr uint64_t kMaxTilesB = kMaxValues / kBTile;
 constexpr uint64_t kGbOffset = 256;
 constexpr uint64_t kTgOffset = kGbOffset + 256 * kMaxSeg * 4;
-constexpr uint64_t kStatusOffset = (kTgOffset + (kMaxTilesB + 1) * 4 + 255) & ~uint64_t(255);
+constexpr uint64_t kChunkHistOffset = (kTgOffset + (kMaxTilesB + 1) * 4 + 255) & ~uint64_t(255);
+constexpr uint64_t kChunkOffOffset = kChunkHistOffset + uint64_t(kMaxChunks) * kWideBuckets * 4;
+constexpr uint64_t kStatusOffset = kChunkOffOffset + uint64_t(kMaxChunks) * kWideBuckets * 4;
 __host__ __device__ inline uint64_t status_words(uint64_t n) {
   uint64_t w = ceil_div(n, kLegacyWideTile) * kWideBuckets;
   w = umax(w, ceil_div(n, kLegacyByteTile) * 256);
@@ -194,6 +222,8 @@ struct SortArgs {
   uint64_t* status;             // look-back statuses (status buffer + 256)
   uint32_t* gb;                 // compact mode: segment starts (256 x nseg)
   uint32_t* tile_group;         // compact mode: group of each pass-B tile's first element
+  const uint32_t* chunk_off;    // first pass: per-chunk digit offsets (kMaxChunks x 2048)
+  uint32_t nchunk;              // chunks of the first pass
 };
 
 // wah_pass.cu: the sort stage's dispatcher.  legacy = 1 (sort_pairs, which

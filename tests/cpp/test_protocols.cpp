@@ -102,7 +102,18 @@ TEST("gpu", "protocols: facade overhead has no positive trend in n (check 6)") {
     for (std::size_t j = i; j < i + 30; ++j) s += ys[j];
     std::printf("    n %.0f: actor - device %.1f us (mean of 30)\n", xs[i], s / 30 * 1e6);
   }
-  const bench::LinearFit fit = bench::fit_line(xs, ys);
+  // host jitter (a worker descheduled, a page fault in a fresh pinned
+  // block) only ever adds time: fit on the fastest 24 of each n's 30 runs
+  std::vector<double> fx, fy;
+  for (std::size_t i = 0; i < xs.size(); i += 30) {
+    std::vector<double> run(ys.begin() + i, ys.begin() + i + 30);
+    std::sort(run.begin(), run.end());
+    for (int k = 0; k < 24; ++k) {
+      fx.push_back(xs[i]);
+      fy.push_back(run[k]);
+    }
+  }
+  const bench::LinearFit fit = bench::fit_line(fx, fy);
   std::printf("    overhead slope 95%% CI [%.3g, %.3g] s per n\n", fit.slope_low, fit.slope_high);
   CHECK(fit.slope_low <= 0.0);  // one-sided: only a confidently positive slope fails
 }
