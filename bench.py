@@ -578,8 +578,8 @@ def run_ours(args, cfg):
     e2e_sync_ms = (time.perf_counter() - t0) * 1e3
 
     # ---- BASELINE config 2: one-warp kernels raw vs through a compute actor
-    iters = 10000
-    for _ in range(3):  # threads and clocks settle over the first few 10^4-launch rounds
+    iters = 10000 if not args.no_probe else 10
+    for _ in range(3 if not args.no_probe else 0):  # threads and clocks settle over the first few rounds
         rt.dispatch_probe_ex(iters)
     probes = [rt.dispatch_probe_ex(iters) for _ in range(5)]
     pr = sorted(probes, key=lambda x: x["actor_ms"] / x["raw_ms"])[2]  # median of 5 by overhead
@@ -587,10 +587,22 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant stage (algorithmic bytes)
     peak, peak_kind = measured_peaks()
-    passes = 1 if cfg["kind"] == "uniform" and cfg["k"] <= 2048 else 2
+    # the sort's passes follow the plan the device made from the key range
+    # (wah_sort.cu k_plan): range < 2^11 -> one wide pass (keys in, pairs
+    # out: 12N); top 16 bits constant -> the compact passes A (keys in,
+    # packed u32 out: 8N) and B (u32 in, pairs out: 12N); otherwise one
+    # legacy byte pass per varying byte (12N, then 16N each)
+    kmin, kmax = raw.key_range()
+    if kmax - kmin < 2048:
+        sort_alg, sort_what = 12 * n, "wide pass: 4 B keys in, 8 B pairs out"
+    elif (kmin >> 16) == (kmax >> 16):
+        sort_alg, sort_what = 20 * n, "pass A: 4 B keys in, 4 B packed out; pass B: 4 B in, 8 B pairs out"
+    else:
+        nb = sum(1 for b in range(4) if (kmin >> (8 * b)) != (kmax >> (8 * b)))
+        sort_alg, sort_what = 12 * n + 16 * n * (nb - 1), f"{nb} byte passes (u64 ping-pong)"
     alg = {
-        "plan": 4 * n,                                # one read of the keys
-        "sort": 12 * n + 16 * n * (passes - 1),      # keys in + pairs out, then pairs in/out
+        "plan": 4 * n,                                # one read of the keys (+ per-chunk counts, KB)
+        "sort": sort_alg,
         "emit": 8 * n + 4 * W + 8 * D,               # pairs in, words + (start, value) out
         "table": 20 * D,
     }
@@ -631,7 +643,10 @@ def run_ours(args, cfg):
                      "probe_runs": 5, "probe_overheads": [x["actor_ms"] / x["raw_ms"] - 1.0 for x in probes]},
         "roofline": {"bound": "hbm", "kernel_stage": dom, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes": alg[dom]},
+                     "traffic": traffic, "algorithmic_bytes": alg[dom],
+                     "model": sort_what if dom == "sort" else "SURVEY 8(d) per-stage bytes",
+                     "timing": "CUDA events around the stage's launches on the launch stream, mean of the "
+                               "timed builds; per-kernel split in profiles/ (ncu)"},
         "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": e2e_steps,
                 "pipelined": "2 deep: step i+1 upload (H2D) and build overlap step i result copy (D2H on the copy engines)",
@@ -665,6 +680,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 26)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3 line inside the C4 report")
+    ap.add_argument("--no-probe", action="store_true",
+                    help="skip the 5 x 10^4-launch dispatch probe (for ncu launch lists, which profile every launch)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU step (shard meta, all-gather, merge) even at N=1")
     args = ap.parse_args()

@@ -38,8 +38,9 @@
 //      digit counters in shared memory
 //   3. tile digit counts, local scan; global digit bases from the running
 //      chunk offsets (wide, A) or the look-back (B)
-//   4. staging in shared memory in digit order (u32 for wide/A, the final
-//      pair for B)
+//   4. staging in shared memory in digit order (u32: wide digit | local,
+//      A hb | lo | local, B the packed word plus its group when the tile
+//      crosses groups)
 //   5. coalesced scatter of the staged runs
 #include <cuda_runtime.h>
 
@@ -95,7 +96,7 @@ struct PassShape {
   static constexpr int WI = 32 * IPT;  // elements per warp
   static constexpr int TILE = THREADS * IPT;
   static constexpr int LOCAL_BITS = ceil_log2(TILE);
-  using Stage = typename std::conditional<KIND == kPassB, uint64_t, uint32_t>::type;
+  using Stage = uint32_t;  // wide/A: digit | local; B: the packed word (its group in a u16 array beside)
   static_assert(TILE <= 65536 && (TILE & (TILE - 1)) == 0, "ranks ride in 16 bits; tiles are powers of two");
   static_assert(KIND != kPassWide || LOCAL_BITS + kWideMaxBits <= 32, "wide staging packs digit | local");
   static_assert(KIND != kPassA || LOCAL_BITS <= 16, "pass-A staging packs hb | lo | local");
@@ -106,6 +107,8 @@ struct PassMisc {
   uint32_t tile[2];        // pass B: tile taken for iteration parity 0/1
   uint32_t tg[2][2];       // pass B: tile_group[t], tile_group[t+1] per parity
   uint32_t sgb[2][32];     // pass B: group starts inside the tile per parity
+  uint32_t kbg[33];        // pass B: key base (top bits | lo) of the tile's groups
+  uint32_t rbg[33];        // pass B: row base (row_base + seg << 24) of the tile's groups
 };
 
 // Shared memory of one CTA: [in: TILE u32][R: H | S][cnt NB][gbase NB][run NB][Misc]
@@ -115,7 +118,7 @@ struct PassSmem {
   static constexpr int NB = 1 << BITS;
   static constexpr size_t kIn = size_t(SH::TILE) * 4;
   static constexpr size_t kH = size_t(SH::WARPS) * NB * 2;
-  static constexpr size_t kS = size_t(SH::TILE) * sizeof(typename SH::Stage);
+  static constexpr size_t kS = size_t(SH::TILE) * (sizeof(typename SH::Stage) + (KIND == kPassB ? 2 : 0));
   static constexpr size_t kR0 = kH > kS ? kH : kS;
   static constexpr size_t kR = SH::ALIAS ? (kR0 > kIn ? kR0 : kIn) : kR0;
   static constexpr size_t kInOfs = 0;
@@ -137,12 +140,6 @@ __device__ __forceinline__ uint32_t pack16(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(r) : "r"(a), "r"(b));
   return r;
-}
-
-// (lo, hi) to shared memory, in program order (volatile: keeps the
-// scheduler from hoisting a whole unrolled tile's values into registers)
-__device__ __forceinline__ void sts_pair(uint32_t addr, uint32_t lo, uint32_t hi) {
-  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(lo), "r"(hi) : "memory");
 }
 
 // Everything a tile needs besides its index (one per CTA, built once).
@@ -447,7 +444,6 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   constexpr uint32_t TILE = SH::TILE;
   const SortArgs& a = c.a;
   uint16_t* H = reinterpret_cast<uint16_t*>(c.R);
-  uint64_t* S = reinterpret_cast<uint64_t*>(c.R);
   PassMisc* m = c.m;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ts = uint64_t(tile) * TILE;
@@ -487,59 +483,50 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   rank_to_tile<KIND, BITS>(H, x, rk2);
   __syncthreads();  // H dead: S may overwrite it
 
-  // ---- staging: the final (key, row) pair.  The group (lo, seg) of each
-  // element: walk the group starts inside the tile (positions grow with r)
-  {
-    const uint32_t g0 = m->tg[par][0], k = m->tg[par][1] - g0;
+  // ---- staging: the packed word in digit order, and when the tile crosses
+  // groups, each element's group (lo, seg) beside it -- found by walking the
+  // group starts inside the tile (positions grow with r)
+  uint32_t* S32 = reinterpret_cast<uint32_t*>(c.R);
+  uint16_t* G16 = reinterpret_cast<uint16_t*>(S32 + TILE);
+  const uint32_t g0 = m->tg[par][0], k = m->tg[par][1] - g0;
+  if (k <= 32 && threadIdx.x <= k) {  // key and row base of every group of the tile
+    const uint32_t g = g0 + threadIdx.x, lo = g / c.nseg, seg = g - lo * c.nseg;
+    m->kbg[threadIdx.x] = c.kbase | lo;
+    m->rbg[threadIdx.x] = a.row_base + (seg << kSegBits);
+  }
+  if (k == 0) {
+#pragma unroll
+    for (int r = 0; r < IPT; ++r)
+      if (FULL || wofs + r * 32 < tn) S32[(rk2[r >> 1] >> (16 * (r & 1))) & 0xffffu] = x[r];
+  } else {
     const uint32_t* sg = m->sgb[par];
     const uint32_t p0 = uint32_t(ts) + wofs;
-    uint32_t j = 0, nb = 0xffffffffu, kb = 0, rb = 0;
-    auto set_group = [&](uint32_t g) {
-      const uint32_t lo = g / c.nseg, seg = g - lo * c.nseg;
-      kb = c.kbase | lo;
-      rb = a.row_base + (seg << kSegBits);
-    };
-    if (k <= 32) {
-      set_group(g0);
-      if (k > 0) nb = sg[0];
-    }
-    const uint32_t s_base = smem_addr(S);
-    if (k == 0) {  // the whole tile inside one group: (key, row) bases fixed
+    uint32_t j = 0, nb = k <= 32 ? sg[0] : 0u;
 #pragma unroll
-      for (int r = 0; r < IPT; ++r)
-        if (FULL || wofs + r * 32 < tn) {
-          const uint32_t v = x[r];
-          sts_pair(s_base + 8u * ((rk2[r >> 1] >> (16 * (r & 1))) & 0xffffu), kb | ((v >> 24) << 8),
-                   rb + (v & 0xffffffu));
+    for (int r = 0; r < IPT; ++r) {
+      const uint32_t p = p0 + uint32_t(r) * 32;
+      if (k <= 32) {
+        if (p >= nb) {
+          while (j < k && p >= sg[j]) ++j;
+          nb = j < k ? sg[j] : 0xffffffffu;
         }
-    } else {
-#pragma unroll
-      for (int r = 0; r < IPT; ++r) {
-        const uint32_t p = p0 + uint32_t(r) * 32;
-        if (k <= 32) {
-          if (p >= nb) {
-            while (j < k && p >= sg[j]) ++j;
-            nb = j < k ? sg[j] : 0xffffffffu;
-            set_group(g0 + j);
-          }
-        } else {
-          // pathological tile (more than 32 groups start inside it): count
-          // the group starts GB[g0+1 .. g0+k] <= p by binary search
-          uint32_t lo_i = 0, hi_i = k;
-          while (lo_i < hi_i) {
-            const uint32_t mid = (lo_i + hi_i) >> 1;
-            if (__ldg(a.gb + g0 + 1 + mid) <= p)
-              lo_i = mid + 1;
-            else
-              hi_i = mid;
-          }
-          set_group(g0 + lo_i);
+      } else {
+        // pathological tile (more than 32 groups start inside it): count
+        // the group starts GB[g0+1 .. g0+k] <= p by binary search
+        uint32_t lo_i = 0, hi_i = k;
+        while (lo_i < hi_i) {
+          const uint32_t mid = (lo_i + hi_i) >> 1;
+          if (__ldg(a.gb + g0 + 1 + mid) <= p)
+            lo_i = mid + 1;
+          else
+            hi_i = mid;
         }
-        if (FULL || wofs + r * 32 < tn) {
-          const uint32_t v = x[r];
-          sts_pair(s_base + 8u * ((rk2[r >> 1] >> (16 * (r & 1))) & 0xffffu), kb | ((v >> 24) << 8),
-                   rb + (v & 0xffffffu));
-        }
+        j = lo_i;
+      }
+      if (FULL || wofs + r * 32 < tn) {
+        const uint32_t slot = (rk2[r >> 1] >> (16 * (r & 1))) & 0xffffu;
+        S32[slot] = x[r];
+        G16[slot] = uint16_t(j);
       }
     }
   }
@@ -556,11 +543,28 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   }
   __syncthreads();
 
-  // ---- scatter
+  // ---- scatter: the (key, row) pair rebuilt from the packed word
+  if (k == 0) {
+    const uint32_t kb = m->kbg[0], rb = m->rbg[0];
 #pragma unroll 4
-  for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
-    const uint64_t e = S[jj];
-    a.X[c.gbase[(uint32_t(e) >> 8) & 0xffu] + jj] = e;
+    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
+      const uint32_t e = S32[jj], d = e >> 24;
+      a.X[c.gbase[d] + jj] = uint64_t(kb | (d << 8)) | (uint64_t(rb + (e & 0xffffffu)) << 32);
+    }
+  } else {
+    for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
+      const uint32_t e = S32[jj], d = e >> 24, gi = G16[jj];
+      uint32_t kb, rb;
+      if (k <= 32) {
+        kb = m->kbg[gi];
+        rb = m->rbg[gi];
+      } else {
+        const uint32_t g = g0 + gi, lo = g / c.nseg, seg = g - lo * c.nseg;
+        kb = c.kbase | lo;
+        rb = a.row_base + (seg << kSegBits);
+      }
+      a.X[c.gbase[d] + jj] = uint64_t(kb | (d << 8)) | (uint64_t(rb + (e & 0xffffffu)) << 32);
+    }
   }
   if (threadIdx.x == 0) claim_next_b(c, ctr, par);
   __syncthreads();

@@ -198,6 +198,11 @@ class WahBuilder:
         for _, call in self.stage_calls(keys, n, row_base, stream):
             call()
 
+    def key_range(self) -> tuple[int, int]:
+        """(min, max) key of the last build (ndx_wah_counts.min_key/max_key)."""
+        c = self.ctl[4:6].cpu().numpy().view(np.uint32)
+        return int(c[0]), int(c[1])
+
     def counts(self) -> tuple[int, int]:
         c = self.ctl[:6].cpu().numpy().view(np.uint64)
         return int(c[0]), int(c[1])

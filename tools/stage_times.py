@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--ref", action="store_true", help="also the oracle's digest of the same values (slow)")
+    ap.add_argument("--no-flush", action="store_true", help="builds back to back (as bench.py), no L2 flush")
     a = ap.parse_args()
     v = gen.config_values(a.config, a.n or None)
     n = v.size
@@ -35,7 +36,8 @@ def main():
     times = []
     calls = b.stage_calls(keys, n)
     for rep in range(a.reps + 3):
-        flush.zero_()
+        if not a.no_flush:
+            flush.zero_()
         ev[0].record(s)
         for i, (_, call) in enumerate(calls):
             call()

@@ -10,8 +10,8 @@ import os
 import subprocess
 import sys
 
-STAGE = {"k_hist": "plan", "k_plan": "plan", "k_hist_hi": "plan", "k_pass": "sort", "k_emit": "emit",
-         "k_table": "table"}
+STAGE = {"k_hist": "plan", "k_plan": "plan", "k_hist_hi": "plan", "k_chunk_scan": "plan", "k_pass": "sort",
+         "k_tma_pass": "sort", "k_pass_bytes": "sort", "k_set_row_hi": "sort", "k_emit": "emit", "k_table": "table"}
 
 
 def kernels(rep):
