@@ -164,12 +164,15 @@ def dist_setup(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        # communicator lines on stderr (stdout carries exactly one JSON line)
+        # NCCL runs inside the C++ runtime (libndactor dlopens it); its
+        # communicator lines go to stderr (stdout carries one JSON line).
+        # torch.distributed (gloo, CPU) only bootstraps: the NCCL id, host
+        # barriers, the max over ranks.
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if args.impl == "ours":
             torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo", rank=rank, world_size=world)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     return world, rank, local
 
 
@@ -260,140 +263,174 @@ def run_reference(args, cfg):
     return 0
 
 
+def json_stdout():
+    """The one JSON line goes to the real stdout; anything native code prints
+    there (NCCL's banner) is sent to stderr instead."""
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    return out
+
+
 def run_sharded(args, cfg, world, rank, local):
-    """N > 1: one process per GPU.  The global column is the concatenation of
-    the ranks' shards (31-aligned bounds over world*n values, each shard
-    generated from seed 42+rank); a step is the local build with global row
-    ids + shard metadata + NCCL all-gather of the metadata + the merge plan +
-    each rank writing its pieces into final form in the merged word array.
-    The gather of all words to rank 0 is timed once, separately."""
+    """N > 1 (or --force-sharded): one process per GPU.  The column is split
+    into 31-aligned row shards; each step, on every rank and stream-ordered
+    on its GPU with no host round trip (include/ndactor/wah_dist.hpp):
+      1. the shard's build through the shard chain of compute actors
+         (plan * sort * emit * table * meta, global row ids);
+      2. one NCCL group (from the C++ runtime): all-gather of every shard's
+         counts and per-value metadata;
+      3. the boundary merge plan on the GPU (SURVEY App. B), replicated;
+      4. the word exchange as one kernel: each rank copies its owned value
+         range of the merged words straight out of the other GPUs' word
+         buffers over NVLink.
+    `value` times steps 1-4.  The gather of the whole index to rank 0 (the
+    same step with rank 0 pulling every word) is timed beside it.
+    Scaling: strong by default (the config's column split over the ranks:
+    C4 = 2^28 values in total); --scaling weak gives every rank the config's
+    size (total rows must stay below 2^31: the index format's u32 offsets)."""
     import torch
     import torch.distributed as dist
 
     from paper_1709_07781_b200 import shard
+    from paper_1709_07781_b200.runtime import DistBuild, Runtime
 
-    dev = torch.device("cuda", local)
-    n = args.n or cfg["n"]
-    bounds = shard.shard_bounds(world * n, world).astype(np.int64)
+    jout = json_stdout()
+    strong = args.scaling == "strong"
+    n_total = (args.n or cfg["n"]) * (1 if strong else world)
+    if n_total >= 1 << 31:
+        raise SystemExit(f"{n_total} rows: a build takes fewer than 2^31 (use --scaling strong)")
+    bounds = shard.shard_bounds(n_total, world).astype(np.int64)
     base, n_r = int(bounds[rank]), int(bounds[rank + 1] - bounds[rank])
-    host_keys = torch.empty(n_r, dtype=torch.int32, pin_memory=True)
-    gen_values(cfg, n_r, rank, host_keys.numpy().view(np.uint32))
+    local_cap = int(np.max(np.diff(bounds)))
+    dev = torch.device("cuda", local)
+    host_keys = torch.empty(max(n_r, 1), dtype=torch.int32, pin_memory=True)
+    if strong:  # one global column: every rank makes the stream and keeps its shard
+        col = gen_values(cfg, n_total, 0)
+        host_keys.numpy().view(np.uint32)[:n_r] = col[base:base + n_r]
+        del col
+    else:
+        gen_values(cfg, n_r, rank, host_keys.numpy().view(np.uint32))
     keys = host_keys.to(dev)
-    sb = shard.ShardBuilder(n_r, device=local)
-    stream = torch.cuda.current_stream()
-    state = {}
 
-    def step(k):
-        W, D, meta_d = sb.build(k, n_r, base)
-        padded, sizes = shard.exchange_meta_device(meta_d, D)
-        entries, pieces, nent, total = shard.plan_merge_device(padded, sizes)
-        state.update(W=W, D=D, entries=entries, pieces=pieces, total=total, nent=nent,
-                     cap=padded.shape[1] // 8, sizes=sizes)
+    rt = Runtime(device=local)
+    obj = [DistBuild.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    meta_cap = 1 << 16 if cfg["k"] <= 1 << 16 else max(1 << 16, local_cap)
+    d = DistBuild(rt, rank, world, obj[0], local_cap, meta_cap, 2 * n_total + 64)
+    rts = torch.cuda.ExternalStream(rt.stream, device=dev)
 
     def barrier():
+        rt.synchronize()
         torch.cuda.synchronize(dev)
         dist.barrier()
 
     def max_over_ranks(x):
-        t = torch.tensor([x], device=dev)
+        t = torch.tensor([float(x)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def timed(steps, gather):
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(rts)
+        for _ in range(steps):
+            d.step(keys.data_ptr(), n_r, base, gather_all=gather and rank == 0)
+        rt.synchronize()  # every stage issued (actor hops) and done
+        a1.record(rts)
+        a1.synchronize()
+        t = a0.elapsed_time(a1) / steps
+        barrier()
+        return max_over_ranks(t)
 
     W_ = max(args.warmup, 3)
     K = args.steps
     for _ in range(W_):
-        step(keys)
+        d.step(keys.data_ptr(), n_r, base)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    barrier()
-    a0 = torch.cuda.Event(enable_timing=True)
-    a1 = torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    for _ in range(K):
-        step(keys)
-    a1.record(stream)
-    barrier()
+    ms = timed(K, False)
     clk = clocks.stop()
-    ms = max_over_ranks(a0.elapsed_time(a1) / K)
-    total_values = world * n
-    value = total_values / (ms * 1e-3)
+    value = n_total / (ms * 1e-3)
 
-    # the gathered index on rank 0 (words over NVLink, then all pieces placed)
-    out = torch.empty(max(state["total"], 1), dtype=torch.int32, device=dev) if rank == 0 else None
-    barrier()
-    g0 = time.perf_counter()
-    staged = shard.gather_words(sb.words[: state["W"]], dst=0)
+    # results of the last owned-slice step: totals, bounds; then the gather
+    from paper_1709_07781_b200 import ndx
+    L = ndx.load()
+
+    def read_totals():
+        o = d.outputs()
+        tot = np.zeros(4, np.uint64)
+        bnd = np.zeros(world + 1, np.uint64)
+        ndx.check(L.ndx_memcpy_d2h_async(tot.ctypes.data, o["totals"], 32, None), "d2h")
+        ndx.check(L.ndx_memcpy_d2h_async(bnd.ctypes.data, o["bounds"], 8 * (world + 1), None), "d2h")
+        ndx.check(L.ndx_device_synchronize(), "sync")
+        return o, tot, bnd
+
+    _, tot, bnd = read_totals()
+    owned_ok = int(tot[2]) == 0
+    gather_ms = timed(max(1, min(K, 5)), True)
+    o, tot_g, _ = read_totals()
+    D, W = int(tot_g[0]), int(tot_g[1])
+    check = {"error_flags": int(tot_g[2]), "words": W, "distinct": D}
     if rank == 0:
-        shard.assemble_slots(staged, state["pieces"], state["cap"], state["sizes"], state["total"], out=out)
-    barrier()
-    gather_ms = max_over_ranks((time.perf_counter() - g0) * 1e3)
+        from paper_1709_07781_b200.runtime import index_digest
 
-    # owned slices (SURVEY 8(e) step 3): all-to-all-v by value range, every
-    # rank ends with a contiguous slice of the merged word array.  Reported
-    # beside the step; a failure is recorded in the line, not fatal (the plan
-    # is replicated, so every rank fails alike and none waits on the others).
-    try:
-        cap, sizes = state["cap"], state["sizes"]
-        hp = state["pieces"].cpu().numpy().view(shard.PIECE_DTYPE)[: world * cap].reshape(world, cap)
-        plist = [hp[g, : int(sizes[g])].copy() for g in range(world)]
-        ent = state["entries"].cpu().numpy().view(np.uint32)
-        shard.exchange_owned(sb.words[: state["W"]], ent, plist, state["total"])  # warm (NCCL p2p setup)
-        barrier()
-        o0 = time.perf_counter()
-        reps = 3
-        for _ in range(reps):
-            obounds, owned = shard.exchange_owned(sb.words[: state["W"]], ent, plist, state["total"])
-        barrier()
-        owned_ms = max_over_ranks((time.perf_counter() - o0) * 1e3 / reps)
-        owned_ok = True
-        if rank == 0:  # rank 0's slice against the gathered index
-            owned_ok = bool(torch.equal(owned, out[int(obounds[0]):int(obounds[1])]))
-        ok_t = torch.tensor([1 if owned_ok else 0], device=dev)
-        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
-        owned_ok = bool(ok_t.item())
-        owned_info = {"ms": owned_ms, "what": "all-to-all-v of the final-form words by value-range "
-                      "ownership (pack, NCCL all_to_all_single, place); host-planned from the "
-                      "replicated merge plan, after one warm call, mean of 3 beside the step",
-                      "max_slice_words": int(np.max(np.diff(obounds))), "check_ok": owned_ok}
-    except Exception as ex:  # noqa: BLE001 - reported in the JSON line
-        owned_info = {"error": repr(ex)[:200]}
+        ent = np.zeros(3 * D, np.uint32)
+        words = np.zeros(W, np.uint32)
+        ndx.check(L.ndx_memcpy_d2h_async(ent.ctypes.data, o["entries"], 12 * D, None), "d2h")
+        ndx.check(L.ndx_memcpy_d2h_async(words.ctypes.data, o["slice"], 4 * W, None), "d2h")
+        ndx.check(L.ndx_device_synchronize(), "sync")
+        dg = "%016x" % index_digest(n_total, ent, words)
+        want = golden_digest(cfg, n_total) if strong else None
+        check.update({"digest": dg, "golden": want, "ok": int(tot_g[2]) == 0 and owned_ok and
+                      (want is None or dg == want)})
 
-    # end to end: pinned host keys in, every step; the rank's merged table and
-    # its own words back to the host
+    # end to end: every step uploads this rank's pinned keys; rank 0 reads the
+    # merged table back, every rank its owned slice
     e2e_steps = max(1, min(K, args.e2e_steps))
-    hw = torch.empty(max(state["W"], 1), dtype=torch.int32, pin_memory=True)
+    slice_words = int(bnd[rank + 1] - bnd[rank])
+    hw = torch.empty(max(slice_words, 1), dtype=torch.int32, pin_memory=True)
+    he = torch.empty(max(3 * D, 1), dtype=torch.int32, pin_memory=True)
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         kk = host_keys.to(dev, non_blocking=True)
-        step(kk)
-        hw[: state["W"]].copy_(sb.words[: state["W"]], non_blocking=True)
-        torch.cuda.synchronize(dev)
+        torch.cuda.current_stream(dev).synchronize()
+        d.step(kk.data_ptr(), n_r, base)
+        rt.synchronize()
+        oo = d.outputs()
+        ndx.check(L.ndx_memcpy_d2h_async(hw.data_ptr(), oo["slice"], 4 * slice_words, None), "d2h")
+        if rank == 0:
+            ndx.check(L.ndx_memcpy_d2h_async(he.data_ptr(), oo["entries"], 12 * D, None), "d2h")
+        ndx.check(L.ndx_device_synchronize(), "sync")
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": W_, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": W_, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "values_per_gpu": n, "keys": cfg["k"],
+        "config": {"workload": cfg["desc"] + (f" -- {n_total} values split over {world} GPUs" if strong else
+                                               f" -- {n_r} values per GPU"),
+                   "values_total": n_total, "values_per_gpu": n_r, "keys": cfg["k"],
                    "distribution": "zipf s=1" if cfg["kind"] == "zipf" else "uniform",
-                   "l2": "inputs larger than L2 (4 B keys x values per GPU > 126 MB)",
-                   "parallelism": f"row shards x{world} (31-aligned), NCCL metadata all-gather, "
-                                  f"boundary merge (SURVEY App. B)",
-                   "words": state["total"], "distinct": state["nent"],
-                   "path": "per-rank 4-stage build (global row ids) + shard metadata kernel + NCCL "
-                           "all-gather of the metadata + merge plan on the GPU (every rank knows where "
-                           "each of its words goes); the gather of all words to rank 0 is timed "
-                           "separately"},
+                   "l2": "inputs larger than L2" if n_r * 4 > 126 << 20 else "inputs may fit L2 (strong scaling)",
+                   "parallelism": f"row shards x{world} (31-aligned), NCCL all-gather of the shard metadata, "
+                                  f"merge plan on the GPU, owned-slice word exchange over NVLink peer memory",
+                   "words": W, "distinct": D,
+                   "path": "per rank: shard chain of compute actors (plan*sort*emit*table*meta) -> NCCL group "
+                           "all-gather (C++ runtime) -> ndx_dist_plan -> ndx_dist_pull (one kernel reading the "
+                           "other GPUs' words); no host round trip inside a step"},
         "gather_to_rank0_ms": gather_ms,
-        "owned_slices": owned_info,
-        "e2e": {"value": total_values / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
-                "d2h_bytes_per_step": 4 * state["W"], "ms_per_step": e2e_ms},
+        "result_check": check,
+        "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
+                "d2h_bytes_per_step": 4 * slice_words + (12 * D if rank == 0 else 0), "ms_per_step": e2e_ms},
         "gpu_launches": 13 * K,
         "clocks": clk,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=jout, flush=True)
+    d.close()
+    rt.close()
     dist.destroy_process_group()
     return 0
 
@@ -684,6 +721,8 @@ def main():
                     help="skip the 5 x 10^4-launch dispatch probe (for ncu launch lists, which profile every launch)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU step (shard meta, all-gather, merge) even at N=1")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N > 1: the config's column split over the GPUs (strong) or per GPU (weak)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

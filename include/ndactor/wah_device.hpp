@@ -58,6 +58,15 @@ struct IndexStages {
 
 IndexStages spawn_index_stages(ActorSystem& sys, Device& dev, std::uint32_t row_base = 0);
 
+/// The multi-GPU build's local chain: plan, sort, emit,
+/// table and the shard metadata stage, row ids from `row_base`.
+/// {keys, wbuf} -> {cfg, wbuf (the words), entries, meta (meta_cap records)}.
+struct ShardStages {
+  ActorHandle plan, sort, emit, table, meta;
+  ActorHandle chain;  // meta * table * emit * sort * plan
+};
+ShardStages spawn_shard_stages(ActorSystem& sys, Device& dev, std::uint32_t row_base, std::uint32_t meta_cap);
+
 /// Device-resident result of the chain.
 struct DeviceIndex {
   std::uint32_t row_count = 0;

@@ -111,6 +111,25 @@ int ndactor_merge_plan(uint32_t shards, const ndx_shard_meta* metas, const uint6
 uint64_t ndactor_index_digest(uint32_t row_count, const uint32_t* entries, uint64_t n_entries,
                               const uint32_t* words, uint64_t n_words);
 
+/* The multi-GPU build behind the actor API (include/ndactor/wah_dist.hpp):
+ * one ndactor_dist per rank (one process per GPU), NCCL loaded by the
+ * runtime.  Rank 0 makes the id, every rank gets a copy (any host channel),
+ * then every rank calls ndactor_dist_create (collective).  A step enqueues
+ * the shard build, the metadata all-gather, the merge plan and the word
+ * exchange on the runtime stream and returns; ndactor_dist_outputs gives the
+ * device results: totals {D, W, error flags, records}, bounds[0..G], the
+ * merged (value, offset, length) table (replicated), the rank's slice of
+ * the merged words [bounds[rank], bounds[rank+1]) (after a gather_all step:
+ * all W words, on every rank that asked), and the rank's local words. */
+typedef struct ndactor_dist ndactor_dist;
+int ndactor_nccl_unique_id(uint8_t* id128);
+int ndactor_dist_create(ndactor_runtime* rt, int rank, int nranks, const uint8_t* id128, uint64_t local_cap,
+                        uint32_t meta_cap, uint64_t slice_cap, ndactor_dist** out);
+int ndactor_dist_step(ndactor_dist* d, const uint32_t* d_keys, uint64_t n_local, uint64_t row_base, int gather_all);
+int ndactor_dist_outputs(ndactor_dist* d, uint64_t** d_totals, uint64_t** d_bounds, uint32_t** d_entries,
+                         uint32_t** d_slice, uint32_t** d_local_words);
+void ndactor_dist_destroy(ndactor_dist* d);
+
 /* "WAH1" index file (p/core/src/wah_index_io.cpp:30-87). */
 int ndactor_write_index_file(const char* path, uint32_t row_count, const uint32_t* entries,
                              uint64_t n_entries, const uint32_t* words, uint64_t n_words);

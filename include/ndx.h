@@ -44,6 +44,13 @@ int ndx_abi_version(void);
 int ndx_device_count(int* count);
 int ndx_device_open(int ordinal);           /* cudaSetDevice + mempool setup */
 int ndx_device_bind(int ordinal);           /* cudaSetDevice only (per host thread) */
+/* cudaMalloc'd memory other processes can map (CUDA IPC, 64-byte handles):
+ * the multi-GPU build reads peer shards' words over NVLink. */
+int ndx_malloc_shared(void** p, size_t bytes);
+int ndx_free_shared(void* p);
+int ndx_ipc_handle(const void* p, void* handle64);
+int ndx_ipc_open(const void* handle64, void** p);
+int ndx_ipc_close(void* p);
 int ndx_device_sm_count(int ordinal, int* sms);
 int ndx_device_synchronize(void);
 
@@ -189,6 +196,11 @@ typedef struct {
 int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
                        uint64_t n_entries, const uint32_t* d_words, ndx_shard_meta* d_meta,
                        void* stream);
+/* The same with the value count read from the device (d_ctl's
+ * ndx_wah_counts) and at most `cap` records written (no host round trip). */
+int ndx_wah_shard_meta_dev(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
+                           const void* d_ctl, uint64_t cap, const uint32_t* d_words, ndx_shard_meta* d_meta,
+                           void* stream);
 /* The merge plan on the device (same result as ndactor_merge_plan): shard
  * g's records at d_metas + g*stride, h_counts[g] of them (host array,
  * shards <= 64).  Writes the merged (value, offset, length) entries and one
@@ -205,6 +217,27 @@ int ndx_wah_assemble_slots(const uint32_t* const* h_src, uint32_t shards, const 
 /* Copies every piece to out (the merged words). */
 int ndx_wah_assemble(const uint32_t* d_src, const ndx_piece* d_pieces, uint64_t n_pieces,
                      uint32_t* d_out, void* stream);
+
+/* The per-step device work of the multi-GPU build with the
+ * shard counts on the device -- no host round trip between the metadata
+ * all-gather and the word exchange.  d_metas: shard g's records in slots
+ * [g*cap, g*cap + d_counts[g].distinct) (the all-gathered ndx_wah_counts of
+ * every shard).  Writes the merged (value, offset, length) table, the pieces
+ * in merged (destination) order with the source shard in `pad`, d_totals
+ * {D, W, error flags (1 empty body, 2 overlapping shards, 4 metadata
+ * capacity exceeded, 8 slice capacity exceeded), records} and the G+1 owner
+ * bounds (rank h owns words [b_h, b_h+1), cut at value boundaries). */
+size_t ndx_dist_plan_scratch_bytes(uint32_t shards, uint64_t cap);
+int ndx_dist_plan(const ndx_shard_meta* d_metas, uint64_t cap, const ndx_wah_counts* d_counts, uint32_t shards,
+                  uint32_t* d_entries, ndx_piece* d_merged, uint64_t* d_totals, uint64_t* d_bounds,
+                  void* d_scratch, void* stream);
+/* Rank `rank`'s owned slice of the merged words (all_words: the whole
+ * array), copied from every shard's words; h_shard_words[g] may point into
+ * another GPU's memory (IPC-mapped, read over NVLink).  out_cap: capacity of
+ * d_out in words; out_hint: expected slice size (grid sizing). */
+int ndx_dist_pull(const uint32_t* const* h_shard_words, uint32_t shards, const ndx_piece* d_merged,
+                  uint64_t max_records, uint64_t* d_totals, const uint64_t* d_bounds, uint32_t rank, int all_words,
+                  uint32_t* d_out, uint64_t out_cap, uint64_t out_hint, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Device primitives behind the reference's public WAH device API

@@ -65,7 +65,7 @@ def build_ndactor(force: bool = False) -> str:
     if force or _stale(out, deps + [os.path.join(LIB, "libndx.so")]):
         cxx = os.environ.get("CXX", "g++")
         _run([cxx, "-std=c++20", "-O2", "-g", "-fPIC", "-shared", "-pthread", "-I" + INC,
-              "-o", out, *srcs, "-L" + LIB, "-lndx", "-Wl,-rpath,$ORIGIN"])
+              "-o", out, *srcs, "-L" + LIB, "-lndx", "-ldl", "-Wl,-rpath,$ORIGIN"])
     return out
 
 

@@ -51,6 +51,26 @@ int ndx_device_open(int ordinal) {
 
 int ndx_device_bind(int ordinal) { return cudaSetDevice(ordinal); }
 
+int ndx_malloc_shared(void** p, size_t bytes) {
+  if (!p) return NDX_E_INVALID;
+  return cudaMalloc(p, bytes ? bytes : 1);
+}
+int ndx_free_shared(void* p) { return cudaFree(p); }
+int ndx_ipc_handle(const void* p, void* handle64) {
+  if (!p || !handle64) return NDX_E_INVALID;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(p));
+  if (!e) memcpy(handle64, &h, sizeof h);
+  return e;
+}
+int ndx_ipc_open(const void* handle64, void** p) {
+  if (!handle64 || !p) return NDX_E_INVALID;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  return cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
+}
+int ndx_ipc_close(void* p) { return cudaIpcCloseMemHandle(p); }
+
 int ndx_device_sm_count(int ordinal, int* sms) {
   if (!sms) return NDX_E_INVALID;
   return cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, ordinal);

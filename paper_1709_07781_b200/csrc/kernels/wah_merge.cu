@@ -62,6 +62,33 @@ __global__ void k_shard_meta(const uint64_t* __restrict__ pairs, uint64_t n,
   }
 }
 
+// The same with the value count on the device (ctl's ndx_wah_counts) and a
+// capacity: at most `cap` records are written (the plan flags a shard whose
+// count exceeds it).
+__global__ void k_shard_meta_dev(const uint64_t* __restrict__ pairs, uint64_t n,
+                                 const uint32_t* __restrict__ entries, const ndx_wah_counts* counts,
+                                 uint64_t cap, const uint32_t* __restrict__ words,
+                                 ndx_shard_meta* __restrict__ meta) {
+  const uint64_t D = umin<uint64_t>(counts->distinct, cap);
+  for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < D;
+       d += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = entries[3 * d], off = entries[3 * d + 1], len = entries[3 * d + 2];
+    const uint64_t lo = lower_key(pairs, n, v);
+    const uint64_t hi = v == 0xffffffffu ? n : lower_key(pairs, n, v + 1);
+    ndx_shard_meta m;
+    m.value = v;
+    m.f = uint32_t(__ldg(pairs + lo) >> 32) / kChunkBits;
+    m.l = uint32_t(__ldg(pairs + hi - 1) >> 32) / kChunkBits;
+    m.skip = is_zero_fill(words[off]) ? 1u : 0u;
+    m.body_off = off + m.skip;
+    m.body_len = len - m.skip;
+    const uint32_t first = words[m.body_off], last = words[m.body_off + m.body_len - 1];
+    m.a = is_ones_fill(first) ? fill_chunks(first) : 0u;
+    m.z = is_ones_fill(last) ? fill_chunks(last) : 0u;
+    meta[d] = m;
+  }
+}
+
 // One warp per piece: the optional lead word, then src_len words copied from
 // the piece's shard words (already offset into the staging buffer).
 __global__ void k_assemble(const uint32_t* __restrict__ src, const ndx_piece* __restrict__ pieces,
@@ -94,6 +121,16 @@ int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_en
   const int grid = int(umin<uint64_t>((n_entries + 255) / 256, 4096));
   k_shard_meta<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_pairs, n, d_entries,
                                                                      n_entries, d_words, d_meta);
+  return cudaGetLastError();
+}
+
+int ndx_wah_shard_meta_dev(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
+                           const void* d_ctl, uint64_t cap, const uint32_t* d_words, ndx_shard_meta* d_meta,
+                           void* stream) {
+  if (!d_pairs || !d_entries || !d_ctl || !d_words || !d_meta || n == 0 || cap == 0) return NDX_E_INVALID;
+  const int grid = int(umin<uint64_t>((cap + 255) / 256, 148 * 8));
+  k_shard_meta_dev<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_pairs, n, d_entries, static_cast<const ndx_wah_counts*>(d_ctl), cap, d_words, d_meta);
   return cudaGetLastError();
 }
 

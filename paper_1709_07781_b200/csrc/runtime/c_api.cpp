@@ -2,6 +2,7 @@
 #include "ndactor_c.h"
 
 #include <chrono>
+#include <stdexcept>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -11,6 +12,8 @@
 #include <thread>
 
 #include "ndactor/compute_actor.hpp"
+#include "ndactor/wah_dist.hpp"
+#include "nccl_comm.hpp"
 #include "ndactor/wah_device.hpp"
 #include "ndactor/wah_io.hpp"
 #include "ndactor/wah_shard.hpp"
@@ -482,6 +485,64 @@ uint64_t ndactor_index_digest(uint32_t row_count, const uint32_t* entries, uint6
   if (n_entries) bytes(entries, 12 * n_entries);  // little-endian host
   if (n_words) bytes(words, 4 * n_words);
   return h;
+}
+
+// ---- multi-GPU build (include/ndactor/wah_dist.hpp) ------------------------
+
+struct ndactor_dist {
+  ndactor_runtime* rt;
+  std::unique_ptr<wah::DistBuild> build;
+};
+
+int ndactor_nccl_unique_id(uint8_t* id128) {
+  return guarded([&] {
+    if (!id128) throw std::invalid_argument("null id buffer");
+    const detail::NcclId id = detail::NcclComm::unique_id();
+    std::memcpy(id128, id.data(), id.size());
+    return 0;
+  });
+}
+
+int ndactor_dist_create(ndactor_runtime* rt, int rank, int nranks, const uint8_t* id128, uint64_t local_cap,
+                        uint32_t meta_cap, uint64_t slice_cap, ndactor_dist** out) {
+  return guarded([&] {
+    if (!rt || !id128 || !out) throw std::invalid_argument("null argument");
+    detail::NcclId id;
+    std::memcpy(id.data(), id128, id.size());
+    auto d = std::make_unique<ndactor_dist>();
+    d->rt = rt;
+    d->build = std::make_unique<wah::DistBuild>(*rt->sys, *rt->dev, rank, nranks, id, local_cap, meta_cap, slice_cap);
+    *out = d.release();
+    return 0;
+  });
+}
+
+int ndactor_dist_step(ndactor_dist* d, const uint32_t* d_keys, uint64_t n_local, uint64_t row_base, int gather_all) {
+  return guarded([&] {
+    if (!d || !d_keys) throw std::invalid_argument("null argument");
+    d->build->step(d_keys, n_local, row_base, gather_all != 0);
+    return 0;
+  });
+}
+
+int ndactor_dist_outputs(ndactor_dist* d, uint64_t** d_totals, uint64_t** d_bounds, uint32_t** d_entries,
+                         uint32_t** d_slice, uint32_t** d_local_words) {
+  return guarded([&] {
+    if (!d) throw std::invalid_argument("null argument");
+    if (d_totals) *d_totals = const_cast<uint64_t*>(d->build->totals());
+    if (d_bounds) *d_bounds = const_cast<uint64_t*>(d->build->bounds());
+    if (d_entries) *d_entries = const_cast<uint32_t*>(d->build->entries());
+    if (d_slice) *d_slice = const_cast<uint32_t*>(d->build->slice());
+    if (d_local_words) *d_local_words = const_cast<uint32_t*>(d->build->local_words());
+    return 0;
+  });
+}
+
+void ndactor_dist_destroy(ndactor_dist* d) {
+  try {
+    delete d;
+  } catch (...) {
+  }
 }
 
 int ndactor_shard_bounds(uint64_t n, uint32_t shards, uint64_t* bounds) {

@@ -301,6 +301,106 @@ IndexStages spawn_index_stages(ActorSystem& sys, Device& dev, std::uint32_t row_
   return st;
 }
 
+// ------------------------------------------------------ shard chain -----
+//
+// The multi-GPU build's local chain: the same plan, sort, emit and table
+// kernels with the shard's global row base, but
+//   * the words land in a caller buffer that travels with the message (a
+//     cudaMalloc'd buffer other GPUs map over NVLink), and
+//   * the sorted pairs travel on to a fifth stage, the shard metadata
+//     (ndx_wah_shard_meta_dev: per value its first/last chunk and end fills,
+//     at most meta_cap records, the count read on the device).
+// {keys, wbuf} -> plan -> sort -> emit -> table -> meta -> {cfg, wbuf, entries, meta}
+
+ShardStages spawn_shard_stages(ActorSystem& sys, Device& dev, std::uint32_t row_base, std::uint32_t meta_cap) {
+  auto ws = workspace_for(dev);
+  const std::size_t ctl_words = ndx_wah_ctl_bytes() / 4;
+  const NdRange one = NdRange::linear(1, 1);
+  const ArgSpec fwd = ArgSpec::in_out(ElemType::u32, ArgMode::ref, ArgMode::ref);
+
+  // plan: {keys, wbuf} -> {cfg, keys, wbuf}
+  ComputeActorSpec plan;
+  plan.kernel = KernelDef("wah_plan", [ws](const LaunchParams& lp) -> int {
+    const std::uint64_t n = lp.len[1];
+    if (n == 0) return 0;
+    ws->ensure(n, lp.stream);
+    return ndx_wah_plan(static_cast<const std::uint32_t*>(lp.ptr[1]), n, lp.ptr[0], ws->status, lp.stream);
+  });
+  plan.args = {ArgSpec::out(ElemType::u32, ctl_words, ArgMode::ref), fwd, fwd};
+  plan.range = one;
+
+  // sort: {cfg, keys, wbuf} -> {cfg, pairs, wbuf}
+  ComputeActorSpec sort;
+  sort.kernel = KernelDef("wah_sort", [ws, row_base](const LaunchParams& lp) -> int {
+    const std::uint64_t n = lp.len[1];
+    if (n == 0) return 0;
+    ws->ensure(n, lp.stream);
+    return ndx_wah_sort(static_cast<const std::uint32_t*>(lp.ptr[1]), n, row_base, lp.ptr[0],
+                        static_cast<std::uint64_t*>(lp.ptr[2]), static_cast<std::uint64_t*>(ws->tmp_pairs),
+                        ws->status, lp.stream);
+  });
+  sort.args = {fwd, ArgSpec::in(ElemType::u32, ArgMode::ref),
+               ArgSpec::out(ElemType::u32, SizeFn{[](const Message& m) { return 2 * ref_len(m, 1); }},
+                            ArgMode::ref)
+                   .uninitialized(),
+               fwd};
+  sort.range = one;
+
+  // emit: {cfg, pairs, wbuf} -> {cfg, pairs, wbuf, vstart, values}
+  ComputeActorSpec emit;
+  emit.kernel = KernelDef("wah_emit", [ws](const LaunchParams& lp) -> int {
+    const std::uint64_t n = lp.len[1] / 2;
+    if (n == 0) return 0;
+    if (lp.len[2] < 2 * n) return NDX_E_INVALID;  // the word buffer holds at most 2 words per value
+    ws->ensure(n, lp.stream);
+    return ndx_wah_emit(static_cast<const std::uint64_t*>(lp.ptr[1]), n, lp.ptr[0],
+                        static_cast<std::uint32_t*>(lp.ptr[2]), static_cast<std::uint32_t*>(lp.ptr[3]),
+                        static_cast<std::uint32_t*>(lp.ptr[4]), ws->emit, lp.stream);
+  });
+  auto n_of_pairs = [](const Message& m) { return ref_len(m, 1) / 2; };
+  emit.args = {fwd, fwd, fwd, ArgSpec::out(ElemType::u32, SizeFn{n_of_pairs}, ArgMode::ref).uninitialized(),
+               ArgSpec::out(ElemType::u32, SizeFn{n_of_pairs}, ArgMode::ref).uninitialized()};
+  emit.range = one;
+
+  // table: {cfg, pairs, wbuf, vstart, values} -> {cfg, pairs, wbuf, entries}
+  ComputeActorSpec table;
+  table.kernel = KernelDef("wah_table", [](const LaunchParams& lp) -> int {
+    const std::uint64_t n = lp.len[3];
+    return ndx_wah_table(static_cast<const std::uint32_t*>(lp.ptr[4]),
+                         static_cast<const std::uint32_t*>(lp.ptr[3]), n, lp.ptr[0],
+                         static_cast<std::uint32_t*>(lp.ptr[5]), lp.stream);
+  });
+  table.args = {fwd, fwd, fwd, ArgSpec::in(ElemType::u32, ArgMode::ref), ArgSpec::in(ElemType::u32, ArgMode::ref),
+                ArgSpec::out(ElemType::u32, SizeFn{[](const Message& m) { return 3 * ref_len(m, 3); }},
+                             ArgMode::ref)
+                    .uninitialized()};
+  table.range = one;
+
+  // meta: {cfg, pairs, wbuf, entries} -> {cfg, wbuf, entries, meta}
+  ComputeActorSpec meta;
+  meta.kernel = KernelDef("wah_shard_meta", [meta_cap](const LaunchParams& lp) -> int {
+    const std::uint64_t n = lp.len[1] / 2;
+    if (n == 0) return 0;
+    return ndx_wah_shard_meta_dev(static_cast<const std::uint64_t*>(lp.ptr[1]), n,
+                                  static_cast<const std::uint32_t*>(lp.ptr[3]), lp.ptr[0], meta_cap,
+                                  static_cast<const std::uint32_t*>(lp.ptr[2]),
+                                  static_cast<ndx_shard_meta*>(lp.ptr[4]), lp.stream);
+  });
+  meta.args = {fwd, ArgSpec::in(ElemType::u32, ArgMode::ref), fwd, fwd,
+               ArgSpec::out(ElemType::u32, std::size_t(meta_cap) * (sizeof(ndx_shard_meta) / 4), ArgMode::ref)
+                   .uninitialized()};
+  meta.range = one;
+
+  ShardStages st;
+  st.plan = spawn_compute(sys, dev, std::move(plan));
+  st.sort = spawn_compute(sys, dev, std::move(sort));
+  st.emit = spawn_compute(sys, dev, std::move(emit));
+  st.table = spawn_compute(sys, dev, std::move(table));
+  st.meta = spawn_compute(sys, dev, std::move(meta));
+  st.chain = st.meta * st.table * st.emit * st.sort * st.plan;
+  return st;
+}
+
 DeviceIndex build_index_device(ActorSystem& sys, const IndexStages& stages, MemRef keys,
                                std::uint32_t row_count) {
   Reply r = sys.request(stages.chain, Message::of(std::move(keys))).await();

@@ -34,6 +34,11 @@ SIGNATURES = [
     ("ndx_device_count", ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     ("ndx_device_open", ctypes.c_int, [ctypes.c_int]),
     ("ndx_device_bind", ctypes.c_int, [ctypes.c_int]),
+    ("ndx_malloc_shared", ctypes.c_int, [ctypes.POINTER(_vp), _sz]),
+    ("ndx_free_shared", ctypes.c_int, [_vp]),
+    ("ndx_ipc_handle", ctypes.c_int, [_vp, _vp]),
+    ("ndx_ipc_open", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    ("ndx_ipc_close", ctypes.c_int, [_vp]),
     ("ndx_device_sm_count", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("ndx_device_synchronize", ctypes.c_int, []),
     ("ndx_stream_create", ctypes.c_int, [ctypes.POINTER(_vp)]),
@@ -73,10 +78,14 @@ SIGNATURES = [
     ("ndx_wah_encode_scratch_bytes", _sz, [_u64]),
     ("ndx_wah_encode", ctypes.c_int, [_vp, _u64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("ndx_wah_shard_meta", ctypes.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
+    ("ndx_wah_shard_meta_dev", ctypes.c_int, [_vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_merge_plan_scratch_bytes", _sz, [_u64]),
     ("ndx_merge_plan", ctypes.c_int, [_vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
     ("ndx_wah_assemble_slots", ctypes.c_int, [_vp, _u32, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_wah_assemble", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
+    ("ndx_dist_plan_scratch_bytes", _sz, [_u32, _u64]),
+    ("ndx_dist_plan", ctypes.c_int, [_vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("ndx_dist_pull", ctypes.c_int, [_vp, _u32, _vp, _u64, _vp, _vp, _u32, ctypes.c_int, _vp, _u64, _u64, _vp]),
     ("ndx_scan_scratch_bytes", _sz, [_u64]),
     ("ndx_scan_exclusive_u32", ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     ("ndx_sort_pairs_scratch_bytes", _sz, [_u64]),

@@ -54,6 +54,13 @@ def load() -> ctypes.CDLL:
                                                   ctypes.POINTER(_u64)]),
             "ndactor_write_index_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, _vp, _u64, _vp, _u64]),
             "ndactor_index_digest": (_u64, [ctypes.c_uint32, _vp, _u64, _vp, _u64]),
+            "ndactor_nccl_unique_id": (ctypes.c_int, [_vp]),
+            "ndactor_dist_create": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _u64, ctypes.c_uint32, _u64,
+                                                   ctypes.POINTER(_vp)]),
+            "ndactor_dist_step": (ctypes.c_int, [_vp, _vp, _u64, _u64, ctypes.c_int]),
+            "ndactor_dist_outputs": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+            "ndactor_dist_destroy": (None, [_vp]),
         }
         for name, (rt, args) in sig.items():
             fn = getattr(lib, name)
@@ -150,3 +157,52 @@ class Runtime:
         _check(self.lib.ndactor_dispatch_probe(self.h, iters, ctypes.byref(raw), ctypes.byref(act),
                                                ctypes.byref(chk)), "dispatch_probe")
         return raw.value, act.value, chk.value
+
+
+class DistBuild:
+    """The multi-GPU build of one rank (include/ndactor/wah_dist.hpp):
+    shard chain through the runtime's actors, NCCL all-gather of the shard
+    metadata, merge plan and word exchange on the GPU -- one call per step,
+    nothing waited for on the host."""
+
+    def __init__(self, rt: Runtime, rank: int, nranks: int, nccl_id: bytes, local_cap: int,
+                 meta_cap: int = 1 << 16, slice_cap: int = 0):
+        self.rt = rt
+        self.lib = rt.lib
+        self.rank, self.nranks = rank, nranks
+        idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = _vp()
+        slice_cap = slice_cap or 2 * local_cap * nranks
+        self.slice_cap = slice_cap
+        _check(self.lib.ndactor_dist_create(rt.h, rank, nranks, ctypes.addressof(idb), local_cap, meta_cap,
+                                            slice_cap, ctypes.byref(h)), "dist_create")
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = load()
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib.ndactor_nccl_unique_id(ctypes.addressof(buf)), "nccl_unique_id")
+        return bytes(buf)
+
+    def step(self, d_keys: int, n: int, row_base: int, gather_all: bool = False) -> None:
+        if row_base < 0 or row_base + n > 1 << 32:
+            raise ValueError("row ids row_base .. row_base + n - 1 must fit in u32")
+        _check(self.lib.ndactor_dist_step(self.h, d_keys, n, row_base, 1 if gather_all else 0), "dist_step")
+
+    def outputs(self) -> dict:
+        t, b, e, sl, lw = _vp(), _vp(), _vp(), _vp(), _vp()
+        _check(self.lib.ndactor_dist_outputs(self.h, ctypes.byref(t), ctypes.byref(b), ctypes.byref(e),
+                                             ctypes.byref(sl), ctypes.byref(lw)), "dist_outputs")
+        return {"totals": t.value, "bounds": b.value, "entries": e.value, "slice": sl.value, "local_words": lw.value}
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.ndactor_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
