@@ -69,6 +69,20 @@ def build_ndactor(force: bool = False) -> str:
     return out
 
 
+def build_verify(force: bool = False) -> str:
+    """libndactor_verify.so: wah::reference_index for the reference's own
+    consumers (ndcli --verify, the acceptance gate).  Not part of the product
+    library: nothing in libndactor/libndx links it."""
+    out = os.path.join(LIB, "libndactor_verify.so")
+    srcs = sorted(glob.glob(os.path.join(CSRC, "verify", "*.cpp")))
+    deps = srcs + [os.path.join(INC, "ndactor", "wah.hpp"), os.path.join(LIB, "libndactor.so")]
+    if force or _stale(out, deps):
+        cxx = os.environ.get("CXX", "g++")
+        _run([cxx, "-std=c++20", "-O2", "-fPIC", "-shared", "-I" + INC, "-o", out, *srcs,
+              "-L" + LIB, "-lndactor", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_cpp_tests(force: bool = False) -> str | None:
     """C++ contract tests (tests/cpp): CPU cases need no GPU; GPU cases use
     real CUDA test kernels and check results against the oracle library."""
@@ -81,10 +95,12 @@ def build_cpp_tests(force: bool = False) -> str | None:
     if not os.path.exists(os.path.join(oracle_dir, "libwah_oracle.so")):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), os.path.join("_build", "libwah_oracle.so")],
                        check=True)
-    deps = srcs + glob.glob(os.path.join(ROOT, "tests", "cpp", "*.hpp")) + [os.path.join(LIB, "libndactor.so")]
+    deps = srcs + glob.glob(os.path.join(ROOT, "tests", "cpp", "*.hpp")) + [os.path.join(LIB, "libndactor.so"),
+                                                                            os.path.join(LIB, "libndactor_verify.so")]
     if force or _stale(out, deps):
         _run([NVCC, *ARCH, "-O1", "-g", "-std=c++20", "-Xcompiler", "-pthread", "-I" + INC,
-              "-o", out, *srcs, "-L" + LIB, "-lndactor", "-lndx", "-L" + oracle_dir, "-lwah_oracle",
+              "-o", out, *srcs, "-L" + LIB, "-lndactor_verify", "-lndactor", "-lndx", "-L" + oracle_dir,
+              "-lwah_oracle",
               "-Xlinker", "-rpath," + LIB + ":" + oracle_dir, "-cudart", "static"])
     return out
 
@@ -92,6 +108,7 @@ def build_cpp_tests(force: bool = False) -> str | None:
 def build_all(force: bool = False) -> None:
     build_ndx(force)
     build_ndactor(force)
+    build_verify(force)
     build_cpp_tests(force)
 
 

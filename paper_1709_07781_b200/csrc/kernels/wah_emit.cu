@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "../../../include/ndx.h"
 #include "common.cuh"
@@ -568,18 +569,18 @@ int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl, uint32_t* d_w
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e) return e;
-  static int grid_for[64] = {};
-  if (!grid_for[dev & 63]) {
-    if ((e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(kEmitSmem))))
-      return e;
+  // per-device launch shape, computed once per device (thread-safe)
+  static int grid_for[64], rc_for[64];
+  static std::once_flag once[64];
+  std::call_once(once[dev & 63], [dev] {
+    int& rc = rc_for[dev & 63];
+    if ((rc = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)))) return;
     int sms = 0, occ = 0;
-    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, kEmitThreads,
-                                                           kEmitSmem)))
-      return e;
+    if ((rc = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return;
+    if ((rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, kEmitThreads, kEmitSmem))) return;
     grid_for[dev & 63] = sms * (occ > 0 ? occ : 1);
-  }
+  });
+  if (rc_for[dev & 63]) return rc_for[dev & 63];
   const uint64_t tiles = emit_tiles(n);
   uint64_t* agg = static_cast<uint64_t*>(d_scratch);
   if ((e = cudaMemsetAsync(agg, 0, tiles * 8, s))) return e;

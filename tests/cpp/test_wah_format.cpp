@@ -93,3 +93,43 @@ TEST("cpu", "wah format: index and value files round-trip") {
   CHECK(read_values_raw("/tmp/ndactor_t.bin") == v);
   CHECK(read_values_text("/tmp/ndactor_t.txt") == v);
 }
+
+// libndactor_verify.so: the reference's CPU ground truth for its own
+// consumers (p/tests/test_wah.cpp:132-160 hand vectors)
+TEST("cpu", "wah verify library: reference_index hand vectors") {
+  const std::vector<uint32_t> a{5, 5, 7, 5};
+  WahIndex ia = reference_index(a);
+  REQUIRE(ia.entries.size() == 2);
+  CHECK(ia.entries[0].value == 5 && ia.entries[0].offset == 0 && ia.entries[0].length == 1);
+  CHECK(ia.entries[1].value == 7 && ia.entries[1].offset == 1 && ia.entries[1].length == 1);
+  CHECK((ia.words == std::vector<uint32_t>{0xbu, 0x4u}));
+  CHECK((reference_index(std::vector<uint32_t>(100, 42)).words == std::vector<uint32_t>{0xc0000003u, 0x7fu}));
+  std::vector<uint32_t> c(100, 3);
+  c[0] = 9;
+  c[99] = 9;
+  WahIndex ic = reference_index(c);
+  REQUIRE(ic.entries.size() == 2 && ic.entries[1].value == 9);
+  const auto b9 = ic.bitmap(ic.entries[1]);
+  CHECK((std::vector<uint32_t>(b9.begin(), b9.end()) == std::vector<uint32_t>{0x1u, 0x80000002u, 0x40u}));
+  const auto b3 = ic.bitmap(ic.entries[0]);
+  CHECK((std::vector<uint32_t>(b3.begin(), b3.end()) == std::vector<uint32_t>{0x7ffffffeu, 0xc0000002u, 0x3fu}));
+  CHECK(reference_index(std::vector<uint32_t>{}).entries.empty());
+}
+
+TEST("cpu", "wah verify library: reference_index matches rows_for on random columns") {
+  std::mt19937 rng(77);
+  for (int it = 0; it < 20; ++it) {
+    std::uniform_int_distribution<uint32_t> card(1, 200), len(1, 5000);
+    const uint32_t k = card(rng);
+    std::uniform_int_distribution<uint32_t> pick(0, k - 1);
+    std::vector<uint32_t> v(len(rng));
+    for (auto& x : v) x = pick(rng) * 7 + 3;
+    WahIndex idx = reference_index(v);
+    for (const IndexEntry& e : idx.entries) {
+      std::vector<uint32_t> want;
+      for (uint32_t r = 0; r < v.size(); ++r)
+        if (v[r] == e.value) want.push_back(r);
+      CHECK(rows_for(idx, e.value) == want);
+    }
+  }
+}
