@@ -130,13 +130,21 @@ __global__ __launch_bounds__(kHistThreads, 1) void k_hist(const uint32_t* __rest
       for (uint64_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) one(keys[j]);
     }
     __syncthreads();
-    uint32_t* out = chunk_hist + uint64_t(c) * kWideBuckets;
+    uint32_t* out = chunk_hist + uint64_t(c) * kChunkHistWords;
     for (int i = threadIdx.x; i < kWideBuckets; i += blockDim.x) {
       uint32_t cnt = 0;
 #pragma unroll
       for (int k = 0; k < kHistCopies; ++k) cnt += hws[k][i];
       out[i] = cnt;
+      hws[0][i] = cnt;
       if (cnt) atomicAdd(&ctl->hist_wide[i], cnt);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {  // byte 0: the 11 bits folded
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kWideBuckets / 256; ++j) cnt += hws[0][i + 256 * j];
+      out[kWideBuckets + i] = cnt;
     }
     __syncthreads();
   }
@@ -316,17 +324,19 @@ __global__ __launch_bounds__(1024) void k_chunk_scan(const Ctl* ctl, const uint3
   const uint32_t d = blockIdx.x * 32 + lane;
   const uint32_t mn = ctl->min_key;
   auto count = [&](uint32_t c) -> uint32_t {
-    const uint32_t* h = chunk_hist + uint64_t(c) * kWideBuckets;
-    if (mode == kModeWide) return __ldg(h + ((d + mn) & (kWideBuckets - 1)));
-    uint32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < kWideBuckets / 256; ++j) s += __ldg(h + d + 256 * j);  // byte 0: the 11 bits folded
-    return s;
+    const uint32_t* h = chunk_hist + uint64_t(c) * kChunkHistWords;
+    return __ldg(h + (mode == kModeWide ? ((d + mn) & (kWideBuckets - 1)) : kWideBuckets + d));
   };
+  // at most kMaxChunks / 32 chunks per warp: every load of the slice in
+  // flight at once
+  constexpr int kPer = int(kMaxChunks / 32);
   const uint32_t c0 = uint32_t(uint64_t(nchunk) * g / 32), c1 = uint32_t(uint64_t(nchunk) * (g + 1) / 32);
+  uint32_t cnt[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) cnt[k] = (d < nb && c0 + k < c1) ? count(c0 + k) : 0u;
   uint32_t sum = 0;
-  if (d < nb)
-    for (uint32_t c = c0; c < c1; ++c) sum += count(c);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) sum += cnt[k];
   part[g][lane] = sum;
   __syncthreads();
   if (g == 0) {
@@ -340,10 +350,12 @@ __global__ __launch_bounds__(1024) void k_chunk_scan(const Ctl* ctl, const uint3
   __syncthreads();
   if (d < nb) {
     uint32_t run = bstart[d] + part[g][lane];
-    for (uint32_t c = c0; c < c1; ++c) {
-      chunk_off[uint64_t(c) * kWideBuckets + d] = run;
-      run += count(c);
-    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (c0 + k < c1) {
+        chunk_off[uint64_t(c0 + k) * kWideBuckets + d] = run;
+        run += cnt[k];
+      }
   }
 }
 

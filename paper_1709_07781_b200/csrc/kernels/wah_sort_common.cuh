@@ -176,7 +176,8 @@ __host__ __device__ inline uint32_t chunk_count(uint64_t n, uint32_t want) {
 // [256 B header: u32 epoch counter, u32 pad, u64 high-water mark]
 // [GB: segment starts of the compact mode, 256 x kMaxSeg u32]
 // [tile_group: pass-B tile -> group of its first element, kMaxTilesB + 1 u32]
-// [chunk counts: kMaxChunks x 2048 u32 (low 11 bits of the key)]
+// [chunk counts: kMaxChunks x (2048 + 256) u32: the low 11 bits of the key,
+//  then byte 0 (the 11 bits folded)]
 // [chunk offsets: kMaxChunks x 2048 u32 (first-pass digit)]
 // [statuses: the pass with the most (tiles x digits), u64 each]
 constexpr uint64_t kMaxValues = 1ull << 31;  // a build takes n < 2^31
@@ -185,7 +186,8 @@ constexpr uint64_t kMaxTilesB = kMaxValues / kBTile;
 constexpr uint64_t kGbOffset = 256;
 constexpr uint64_t kTgOffset = kGbOffset + 256 * kMaxSeg * 4;
 constexpr uint64_t kChunkHistOffset = (kTgOffset + (kMaxTilesB + 1) * 4 + 255) & ~uint64_t(255);
-constexpr uint64_t kChunkOffOffset = kChunkHistOffset + uint64_t(kMaxChunks) * kWideBuckets * 4;
+constexpr uint64_t kChunkHistWords = kWideBuckets + 256;
+constexpr uint64_t kChunkOffOffset = kChunkHistOffset + uint64_t(kMaxChunks) * kChunkHistWords * 4;
 constexpr uint64_t kStatusOffset = kChunkOffOffset + uint64_t(kMaxChunks) * kWideBuckets * 4;
 __host__ __device__ inline uint64_t status_words(uint64_t n) {
   uint64_t w = ceil_div(n, kLegacyWideTile) * kWideBuckets;
