@@ -625,22 +625,26 @@ def run_ours(args, cfg):
     # ---- roofline of the dominant stage (algorithmic bytes)
     peak, peak_kind = measured_peaks()
     # the sort's passes follow the plan the device made from the key range
-    # (wah_sort.cu k_plan): range < 2^11 -> one wide pass (keys in, pairs
-    # out: 12N); top 16 bits constant -> the compact passes A (keys in,
-    # packed u32 out: 8N) and B (u32 in, pairs out: 12N); otherwise one
-    # legacy byte pass per varying byte (12N, then 16N each)
+    # (wah_sort.cu k_plan): range < 2^11 -> one wide pass (keys in, row ids
+    # out: 8N); top 16 bits constant -> the compact passes A (keys in,
+    # packed u32 out: 8N) and B (u32 in, row ids out: 8N) -- both write the
+    # sorted stream in rows form, the emit reads 4 B per value; otherwise one
+    # legacy byte pass per varying byte (12N, then 16N each) and (key, row)
+    # pairs (8 B per value) into the emit
     kmin, kmax = raw.key_range()
+    stream_b = 4
     if kmax - kmin < 2048:
-        sort_alg, sort_what = 12 * n, "wide pass: 4 B keys in, 8 B pairs out"
+        sort_alg, sort_what = 8 * n, "wide pass: 4 B keys in, 4 B row ids out"
     elif (kmin >> 16) == (kmax >> 16):
-        sort_alg, sort_what = 20 * n, "pass A: 4 B keys in, 4 B packed out; pass B: 4 B in, 8 B pairs out"
+        sort_alg, sort_what = 16 * n, "pass A: 4 B keys in, 4 B packed out; pass B: 4 B in, 4 B row ids out"
     else:
         nb = sum(1 for b in range(4) if (kmin >> (8 * b)) != (kmax >> (8 * b)))
         sort_alg, sort_what = 12 * n + 16 * n * (nb - 1), f"{nb} byte passes (u64 ping-pong)"
+        stream_b = 8
     alg = {
         "plan": 4 * n,                                # one read of the keys (+ per-chunk counts, KB)
         "sort": sort_alg,
-        "emit": 8 * n + 4 * W + 8 * D,               # pairs in, words + (start, value) out
+        "emit": stream_b * n + 4 * W + 8 * D,        # stream in, words + (start, value) out
         "table": 20 * D,
     }
     dom = max(stage_ms, key=stage_ms.get)

@@ -85,9 +85,15 @@ int ndx_memcpy_d2d_async(void* d_dst, const void* d_src, size_t bytes, void* str
  * Replaces wah::build_index (p/core/src/wah_builder.cpp:38-307).
  *
  *   S1 plan   keys[n]              -> ctl (key range, histograms, sort plan)
- *   S2 sort   keys[n] + ctl        -> pairs[n]: u64 (key | row << 32), stable
- *                                     by key; row ids made on the fly
- *   S3 emit   pairs + ctl          -> words[<=2n], vstart[<=n], values[<=n],
+ *   S2 sort   keys[n] + ctl        -> the sorted stream (stable by key; row ids
+ *                                     made on the fly) in d_pairs, in one of
+ *                                     two forms chosen on the device:
+ *                                     rows form (keys within 2^16 of each
+ *                                     other): u32 row ids, the values kept in
+ *                                     ctl as the present keys and where each
+ *                                     one's rows begin; pairs form (any other
+ *                                     keys): u64 (key | row << 32)
+ *   S3 emit   stream + ctl         -> words[<=2n], vstart[<=n], values[<=n],
  *                                     ctl.{words, distinct}
  *   S4 table  values, vstart, ctl  -> entries[3*D] (value, offset, length)
  *
@@ -191,9 +197,9 @@ typedef struct {
   uint32_t pad;
 } ndx_piece;
 
-/* meta[d] for each entry d of a local index built by the four stages (pairs
- * are that build's sorted pairs). */
-int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
+/* meta[d] for each entry d of a local index built by the four stages
+ * (d_pairs and d_ctl: that build's sorted stream and control block). */
+int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const void* d_ctl, const uint32_t* d_entries,
                        uint64_t n_entries, const uint32_t* d_words, ndx_shard_meta* d_meta,
                        void* stream);
 /* The same with the value count read from the device (d_ctl's

@@ -317,6 +317,7 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
                                                           uint32_t* __restrict__ vstart,
                                                           uint32_t* __restrict__ values,
                                                           uint64_t* agg, int bulk_ok) {
+  if (ctl->rows_form) return;  // k_emit_rows
   extern __shared__ __align__(16) unsigned char emit_smem[];
   uint64_t* buf0 = reinterpret_cast<uint64_t*>(emit_smem);
   uint32_t* stage = reinterpret_cast<uint32_t*>(buf0 + 2 * kEmitBuf);
@@ -528,6 +529,504 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
   }
 }
 
+// ---- rows form -----------------------------------------------------------------
+// The wide pass and pass B write the sorted stream as row ids only; the
+// values are the present keys in order with the stream position where each
+// begins (ctl->pk / ctl->vs, k_vs).  The emit then reads 4 bytes per element
+// instead of 8, and a tile learns its value heads from a 128-byte record
+// (k_tile_heads) that arrives with its rows by the same bulk copy.  A value
+// head is the only thing the key contributed (wah_builder.cpp:74-75: v
+// differs from the element before); the table's values are pk itself.
+
+constexpr int kRowsHaloR = 4;                              // 16-byte multiple of u32 rows
+constexpr int kRowsBuf = kHaloL + kEmitTile + kRowsHaloR;  // rows per tile buffer
+constexpr int kRecHeads = 60;
+struct __align__(16) TileRec {
+  uint32_t ib, ie;          // the value heads inside the buffer: vs[ib .. ie) (ib == ie: none)
+  uint16_t hp[kRecHeads];   // buffer positions of the first kRecHeads of them
+};
+static_assert(sizeof(TileRec) == 128, "one bulk copy per record");
+// two row buffers, two records, then the words of one tile and the
+// tile-local word offsets of its value heads
+constexpr size_t kEmitRowsSmem =
+    size_t(2 * kRowsBuf) * 4 + 2 * sizeof(TileRec) + size_t(2 * kEmitTile) * 4 + size_t(kEmitTile) * 2;
+
+// The value heads of one tile buffer (positions relative to the buffer's
+// first element, ascending): from the record, or -- a tile with more than
+// kRecHeads heads -- from vs itself.
+struct Heads {
+  const uint16_t* hp;
+  const uint32_t* vs;
+  uint32_t m, ib;
+  int64_t p0;  // stream position of buffer element 0
+  __device__ __forceinline__ uint32_t at(uint32_t k) const {
+    return m <= uint32_t(kRecHeads) ? uint32_t(hp[k]) : uint32_t(int64_t(__ldg(vs + ib + k)) - p0);
+  }
+  // heads at buffer positions < q
+  __device__ __forceinline__ uint32_t below(uint32_t q) const {
+    uint32_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (at(mid) < q)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  }
+};
+
+// Largest t with rows[g+t] == row+t inside the value (g+t < end), given that
+// it holds for t = 30 (stretch_end of the pairs form).
+__device__ __noinline__ uint32_t stretch_end_r(const uint32_t* __restrict__ rows, uint64_t end, uint64_t g,
+                                               uint32_t row) {
+  auto P = [&](uint64_t t) -> bool {
+    if (g + t >= end) return false;
+    const uint64_t rr = uint64_t(row) + t;
+    if (rr > 0xffffffffull) return false;
+    return __ldg(rows + g + t) == uint32_t(rr);
+  };
+  uint64_t lo = 30, hi, step = 32;
+  for (;;) {
+    const uint64_t cand = lo + step;
+    if (!P(cand)) {
+      hi = cand;
+      break;
+    }
+    lo = cand;
+    step <<= 1;
+  }
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (P(mid))
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return uint32_t(lo);
+}
+
+// ones_body of the pairs form: the value's extent [vs[i], vs[i+1]) replaces
+// the key comparisons.
+__device__ __noinline__ uint32_t ones_body_r(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ vs,
+                                             uint32_t nvals, uint64_t e, uint32_t row) {
+  uint32_t lo = 0, hi = nvals;  // vs[lo] <= e < vs[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(vs + mid) <= e)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const uint64_t vb = __ldg(vs + lo), ve = __ldg(vs + lo + 1);
+  if (e >= 61 && row >= 61 && e - 61 >= vb && __ldg(rows + e - 61) == row - 61) return 0;
+  const uint32_t t = stretch_end_r(rows, ve, e - 30, row - 30);
+  return make_fill(true, (t + 1) / kChunkBits);
+}
+
+// Phase 1 of the rows form (span_scan): the value-head bits come from the
+// tile's head list instead of key comparisons.
+template <bool SMALL, bool FULL>
+__device__ __forceinline__ void span_scan_r(const uint32_t* R, const Heads& H, const uint32_t* __restrict__ rows,
+                                            const uint32_t* __restrict__ vs, uint32_t nvals, uint32_t n,
+                                            uint32_t ts, uint32_t li0, Span& s) {
+  const uint32_t q0 = kHaloL + li0;
+  // 7 x 8 B per thread: a 56-byte stride hits distinct bank pairs
+  uint32_t r[kEmitK];
+  const uint2* R2 = reinterpret_cast<const uint2*>(R + q0);
+#pragma unroll
+  for (int p = 0; p < kEmitK / 2; ++p) {
+    const uint2 u = R2[p];
+    r[2 * p] = u.x;
+    r[2 * p + 1] = u.y;
+  }
+  const uint32_t prv = R[q0 - 1], nxt = R[q0 + kEmitK];
+  // value heads at q0 .. q0 + kEmitK (bit kEmitK: the element after the span)
+  uint32_t vb = 0;
+  if (H.m) {
+    for (uint32_t k = H.below(q0); k < H.m; ++k) {
+      const uint32_t h = H.at(k);
+      if (h > q0 + kEmitK) break;
+      vb |= 1u << (h - q0);
+    }
+  }
+  const uint32_t g0 = ts + li0;
+  uint32_t pc = div31<SMALL>(prv);
+  uint32_t hm = 0, vm = 0, gaps = 0, acc = 0;
+#pragma unroll
+  for (int j = 0; j < kEmitK; ++j) {
+    const uint32_t row = r[j], c = div31<SMALL>(row);
+    const uint32_t bp = row - c * kChunkBits;
+    bool vh = (vb >> j) & 1u, h = vh | (c != pc);
+    if (!FULL) {
+      const uint32_t g = g0 + j;
+      const bool valid = g < n;
+      vh = valid & (vh | (g == 0));
+      h = valid & (h | (g == 0));
+    }
+    const uint32_t gap = h ? (vh ? c : c - pc - 1) : 0u;
+    gaps += gap != 0;
+    s.pk[j] = SMALL ? (gap << 5) | bp : gap;
+    hm |= uint32_t(h) << j;
+    vm |= uint32_t(vh) << j;
+    acc = (h ? 0u : acc) | (1u << bp);
+    pc = c;
+  }
+  const bool hN = ((vb >> kEmitK) & 1u) | (div31<SMALL>(nxt) != pc);
+  uint32_t tm;
+  if (FULL) {
+    tm = (hm >> 1) | (uint32_t(hN) << (kEmitK - 1));
+  } else {
+    const uint32_t nvalid = g0 >= n ? 0u : umin(n - g0, uint32_t(kEmitK + 1));
+    const uint32_t valid9 = (1u << nvalid) - 1u;
+    const uint32_t h9 = hm | (uint32_t(hN) << kEmitK);
+    tm = valid9 & ((1u << kEmitK) - 1u) & ((h9 >> 1) | (~valid9 >> 1));
+  }
+  s.hmask = hm;
+  s.vmask = vm;
+  s.tmask = tm;
+  s.acc = acc;
+  s.nwords = gaps + __popc(tm);
+  // first_run_check: the span's first run, begun before the span, all-ones?
+  s.first_body = 1;
+  if (tm != 0 && (hm == 0 || __ffs(tm) < __ffs(hm))) {
+    const uint32_t j = __ffs(tm) - 1, q = q0 + j;
+    const uint32_t row = R[q];
+    if (row - div31<SMALL>(row) * kChunkBits == kChunkBits - 1 && g0 + j >= 30 && R[q - 30] == row - 30) {
+      // same value: no head in [q0, q] (the run has none there), and the
+      // last one before the span at or before q - 30
+      const uint32_t k = H.below(q0);
+      if (k == 0 || H.at(k - 1) <= q - 30) {
+        s.first_body = ones_body_r(rows, vs, nvals, g0 + j, row);
+        if (s.first_body == 0) s.nwords -= 1;
+      }
+    }
+  }
+}
+
+// warp_carry of the rows form: "same value as element wl" is "no value head
+// after q up to wl".
+template <bool SMALL>
+__device__ __forceinline__ uint32_t warp_carry_r(const uint32_t* R, const Heads& H, uint32_t ts, uint32_t wl) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wq = kHaloL + wl;
+  const uint32_t c0 = div31<SMALL>(R[wq]);
+  const uint32_t q = wq - 32 + lane;
+  const uint32_t qrow = R[q], qc = div31<SMALL>(qrow);
+  uint32_t lh = 0;
+  if (H.m) {
+    const uint32_t k = H.below(wq + 1);
+    if (k) lh = H.at(k - 1);
+  }
+  const bool m = (ts + wl + lane >= 32) & (q >= lh) & (qc == c0);
+  return __reduce_or_sync(kFull, m ? 1u << (qrow - qc * kChunkBits) : 0u);
+}
+
+// Phase 2 of the rows form (span_emit): only the heads' word offsets are
+// staged (the values are pk).
+template <bool SMALL>
+__device__ __forceinline__ void span_emit_r(const Span& s, const uint32_t* Rs, uint32_t carry, uint32_t o,
+                                            uint32_t h, uint32_t* stage, uint16_t* ho) {
+  uint32_t sa = smem_addr(stage) + 4u * o;
+  uint32_t acc = carry;
+  auto bit = [&](int j) -> uint32_t {
+    if (SMALL) return 1u << (s.pk[j] & 31u);
+    const uint32_t row = Rs[j];
+    return 1u << (row - (row / kChunkBits) * kChunkBits);
+  };
+  if (s.vmask == 0 && s.first_body == 1) {
+#pragma unroll
+    for (int j = 0; j < kEmitK; ++j) {
+      const uint32_t gap = gap_of<SMALL>(s.pk[j]), b = bit(j);
+      if (gap) {
+        sts_u32(sa, kFillFlag | gap);
+        sa += 4;
+      }
+      acc = ((s.hmask >> j) & 1u) ? b : (acc | b);
+      if ((s.tmask >> j) & 1u) {
+        sts_u32(sa, acc);
+        sa += 4;
+      }
+    }
+    return;
+  }
+  const uint32_t sbase = smem_addr(stage);
+#pragma unroll
+  for (int j = 0; j < kEmitK; ++j) {
+    const uint32_t gap = gap_of<SMALL>(s.pk[j]), b = bit(j);
+    if ((s.vmask >> j) & 1u) {
+      ho[h] = uint16_t((sa - sbase) >> 2);
+      ++h;
+    }
+    if (gap) {
+      sts_u32(sa, kFillFlag | gap);
+      sa += 4;
+    }
+    acc = ((s.hmask >> j) & 1u) ? b : (acc | b);
+    if ((s.tmask >> j) & 1u) {
+      const bool first = (s.hmask & ((2u << j) - 1u)) == 0;
+      const uint32_t body = (first && s.first_body != 1) ? s.first_body : acc;
+      if (body) {
+        sts_u32(sa, body);
+        sa += 4;
+      }
+    }
+  }
+}
+
+// Per emit tile: the aggregate word and the head record's range cleared.
+__global__ void k_tile_prep(uint64_t* agg, TileRec* __restrict__ recs, uint32_t ntiles) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+    agg[t] = 0;
+    *reinterpret_cast<uint2*>(recs + t) = make_uint2(0, 0);
+  }
+}
+
+// The head records, from the heads' side: value head i (stream position P)
+// lies in the buffers of one or two tiles; for each it writes the record's
+// range ends it is (first: ib, last: ie) and its slot among the first
+// kRecHeads (the heads of the buffer before it, counted backwards).  The
+// table's values are the present keys (pk) in order.
+constexpr int kHeadsThreads = 1024;
+__global__ __launch_bounds__(kHeadsThreads) void k_tile_heads(const Ctl* __restrict__ ctl,
+                                                              TileRec* __restrict__ recs, uint32_t ntiles,
+                                                              uint32_t* __restrict__ values) {
+  if (!ctl->rows_form) return;
+  const uint32_t nv = ctl->nvals;
+  const uint32_t i = blockIdx.x * kHeadsThreads + threadIdx.x;
+  if (i >= nv) return;
+  const uint32_t* vs = ctl->vs;
+  values[i] = ctl->pk[i];
+  const int64_t P = vs[i];
+  const int64_t prv = i ? int64_t(vs[i - 1]) : -1;
+  const int64_t nxt = i + 1 < nv ? int64_t(vs[i + 1]) : INT64_MAX;
+  const uint32_t th = uint32_t((P + kHaloL) / kEmitTile);  // the last tile whose buffer starts at or before P
+  for (uint32_t t = th > 0 ? th - 1 : 0; t <= th && t < ntiles; ++t) {
+    const int64_t p0 = int64_t(t) * kEmitTile - kHaloL;
+    if (P < p0 || P >= p0 + kRowsBuf) continue;
+    TileRec* r = recs + t;
+    if (prv < p0) r->ib = i;
+    if (nxt >= p0 + kRowsBuf) r->ie = i + 1;
+    uint32_t k = 0;
+    for (uint32_t j = i; k < uint32_t(kRecHeads) && j > 0 && int64_t(vs[j - 1]) >= p0; --j) ++k;
+    if (k < uint32_t(kRecHeads)) r->hp[k] = uint16_t(P - p0);
+  }
+}
+
+// S3 over the rows form: k_emit's tile schedule, aggregates and write-out
+// (see there); three CTAs per SM fit beside the half-size buffers.
+__global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* __restrict__ rows, uint64_t n,
+                                                               Ctl* ctl, uint32_t* __restrict__ words,
+                                                               uint32_t* __restrict__ vstart,
+                                                               const TileRec* __restrict__ recs, uint64_t* agg,
+                                                               int bulk_ok) {
+  if (!ctl->rows_form) return;
+  extern __shared__ __align__(16) unsigned char emit_smem[];
+  uint32_t* buf0 = reinterpret_cast<uint32_t*>(emit_smem);
+  TileRec* srec = reinterpret_cast<TileRec*>(buf0 + 2 * kRowsBuf);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(srec + 2);
+  uint16_t* ho = reinterpret_cast<uint16_t*>(stage + 2 * kEmitTile);
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ uint32_t s_wt[2][kEmitWarps];
+  __shared__ uint32_t s_rw[kEmitWarps], s_rd[kEmitWarps];
+  __shared__ uint32_t s_tile[2];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t ntiles = uint32_t((n + kEmitTile - 1) / kEmitTile);
+  const uint32_t n32 = uint32_t(n);
+  const bool small_rows = ctl->row_hi < kDiv31FastLimit;
+  const uint32_t* vs = ctl->vs;
+  const uint32_t nvals = ctl->nvals;
+  uint32_t* ctr = &ctl->tile_ctr[0];
+
+  auto by_bulk = [&](uint32_t t) -> bool {
+    return bulk_ok && t > 0 && uint64_t(t + 1) * kEmitTile + kRowsHaloR <= n;
+  };
+  auto bulk_fill = [&](uint32_t t, int b) {  // one thread
+    fence_proxy_async_smem();
+    mbar_expect_tx(&bar[b], kRowsBuf * 4 + uint32_t(sizeof(TileRec)));
+    bulk_g2s(buf0 + b * kRowsBuf, rows + (int64_t(t) * kEmitTile - kHaloL), kRowsBuf * 4, &bar[b]);
+    bulk_g2s(srec + b, recs + t, uint32_t(sizeof(TileRec)), &bar[b]);
+  };
+  auto manual_fill = [&](uint32_t t, int b) {  // all threads
+    uint32_t* dst = buf0 + b * kRowsBuf;
+    const int64_t g0 = int64_t(t) * kEmitTile - kHaloL;
+    for (int j = threadIdx.x; j < kRowsBuf; j += kEmitThreads) {
+      const int64_t g = g0 + j;
+      dst[j] = (g >= 0 && uint64_t(g) < n) ? __ldg(rows + g) : 0u;
+    }
+    if (threadIdx.x < sizeof(TileRec) / 4)
+      reinterpret_cast<uint32_t*>(srec + b)[threadIdx.x] = reinterpret_cast<const uint32_t*>(recs + t)[threadIdx.x];
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    const uint32_t t = atomicAdd(ctr, 1u);
+    s_tile[0] = t;
+    if (t < ntiles && by_bulk(t)) bulk_fill(t, 0);
+  }
+  __syncthreads();
+
+  uint64_t prev_w = 0, prev_d = 0;
+  int64_t prev_tile = -1;
+  int64_t pending = -1;
+  uint32_t phase = 0;
+  Span sp;
+  uint32_t carry_in = 0, excl = 0;
+  for (int it = 0;; ++it) {
+    const int b = it & 1;
+    const uint32_t tile = s_tile[b];
+    const bool has = tile < ntiles;
+    if (!has && pending < 0) break;
+    const bool full = has && by_bulk(tile);
+    const uint32_t* R = buf0 + b * kRowsBuf;  // R[kHaloL + li] = rows[tile * kEmitTile + li]
+    const uint32_t ts = tile * kEmitTile, li0 = threadIdx.x * kEmitK;
+    constexpr int kAggPre = 4;
+    uint64_t pre[kAggPre];
+    const uint64_t agg_lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
+    const uint64_t agg_hi = pending < 0 ? agg_lo : uint64_t(pending);
+#pragma unroll
+    for (int j = 0; j < kAggPre; ++j) {
+      const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
+      pre[j] = a < agg_hi ? ld_relaxed_u64(&agg[a]) : kAggReady;
+    }
+    if (has) {
+      if (full) {
+        mbar_wait(&bar[b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+      } else {
+        manual_fill(tile, b);
+        __syncthreads();
+      }
+      Heads H;
+      H.hp = srec[b].hp;
+      H.vs = vs;
+      H.m = srec[b].ie - srec[b].ib;
+      H.ib = srec[b].ib;
+      H.p0 = int64_t(ts) - kHaloL;
+      // ---- phase 1: counts and carries
+      uint32_t wcarry;
+      if (small_rows) {
+        if (full)
+          span_scan_r<true, true>(R, H, rows, vs, nvals, n32, ts, li0, sp);
+        else
+          span_scan_r<true, false>(R, H, rows, vs, nvals, n32, ts, li0, sp);
+        wcarry = warp_carry_r<true>(R, H, ts, uint32_t(warp) * 32 * kEmitK);
+      } else {
+        if (full)
+          span_scan_r<false, true>(R, H, rows, vs, nvals, n32, ts, li0, sp);
+        else
+          span_scan_r<false, false>(R, H, rows, vs, nvals, n32, ts, li0, sp);
+        wcarry = warp_carry_r<false>(R, H, ts, uint32_t(warp) * 32 * kEmitK);
+      }
+      uint32_t x = (sp.hmask ? 0x80000000u : 0u) | sp.acc;
+      const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, d);
+        const uint32_t z = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) {
+          if (!(x >> 31)) x |= y;
+          incl += z;
+        }
+      }
+      const uint32_t incl_lit = (x & kLiteralMask) | ((x >> 31) ? 0u : wcarry);
+      carry_in = __shfl_up_sync(kFull, incl_lit, 1);
+      if (lane == 0) carry_in = wcarry;
+      excl = incl - cnt;
+      if (lane == 31) s_wt[b][warp] = incl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (has) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kEmitWarps; ++w) tot += s_wt[b][w];
+        st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32));
+      }
+      const uint32_t nt = has ? atomicAdd(ctr, 1u) : ntiles;
+      s_tile[b ^ 1] = nt;
+      if (nt < ntiles && by_bulk(nt)) bulk_fill(nt, b ^ 1);
+    }
+
+    if (pending >= 0) {
+      const int pb = b ^ 1;
+      const uint64_t pt = uint64_t(pending);
+      uint32_t sw = 0, sd = 0;
+#pragma unroll
+      for (int j = 0; j < kAggPre; ++j) {
+        const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
+        if (a >= pt) break;
+        uint64_t s = pre[j];
+        while (!(s & kAggReady)) {
+          __nanosleep(32);
+          s = ld_relaxed_u64(&agg[a]);
+        }
+        sw += uint32_t(s);
+        sd += uint32_t(s >> 32) & 0x7fffffffu;
+      }
+      for (uint64_t j = agg_lo + threadIdx.x + uint64_t(kAggPre) * kEmitThreads; j < pt; j += kEmitThreads) {
+        uint64_t s = ld_relaxed_u64(&agg[j]);
+        while (!(s & kAggReady)) {
+          __nanosleep(32);
+          s = ld_relaxed_u64(&agg[j]);
+        }
+        sw += uint32_t(s);
+        sd += uint32_t(s >> 32) & 0x7fffffffu;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sw += __shfl_xor_sync(kFull, sw, o);
+        sd += __shfl_xor_sync(kFull, sd, o);
+      }
+      if (lane == 0) {
+        s_rw[warp] = sw;
+        s_rd[warp] = sd;
+      }
+      __syncthreads();
+      uint64_t W0 = prev_w, D0 = prev_d;
+      uint32_t tw = 0, td = 0;
+#pragma unroll
+      for (int w = 0; w < kEmitWarps; ++w) {
+        W0 += s_rw[w];
+        D0 += s_rd[w];
+        tw += s_wt[pb][w] >> 16;
+        td += s_wt[pb][w] & 0xffffu;
+      }
+      prev_w = W0;
+      prev_d = D0;
+      prev_tile = int64_t(pt);
+      if (threadIdx.x == 0 && pt == ntiles - 1) {
+        ctl->words = W0 + tw;
+        ctl->distinct = D0 + td;
+      }
+      {
+        uint32_t* const wd = words + W0;
+#pragma unroll 4
+        for (uint32_t j = threadIdx.x; j < tw; j += kEmitThreads) wd[j] = stage[j];
+      }
+      for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) vstart[D0 + j] = uint32_t(W0 + ho[j]);
+    }
+    __syncthreads();
+
+    if (has) {
+      uint32_t wbase = 0;
+#pragma unroll
+      for (int w = 0; w < kEmitWarps; ++w) wbase += w < warp ? s_wt[b][w] : 0u;
+      const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
+      const uint32_t* Rs = R + kHaloL + li0;
+      if (small_rows)
+        span_emit_r<true>(sp, Rs, carry_in, o, h, stage, ho);
+      else
+        span_emit_r<false>(sp, Rs, carry_in, o, h, stage, ho);
+    }
+    pending = has ? int64_t(tile) : -1;
+  }
+}
+
 // S4: (value, offset, length) rows (wah_builder.cpp:238-257).
 __global__ void k_table(const uint32_t* __restrict__ values, const uint32_t* __restrict__ vstart,
                         const Ctl* ctl, uint32_t* __restrict__ entries) {
@@ -558,7 +1057,12 @@ using namespace ndx;
 
 extern "C" {
 
-size_t ndx_wah_emit_scratch_bytes(uint64_t n) { return size_t(emit_tiles(n) + 1) * 8 + 256; }
+// scratch: the tiles' aggregate words, then (128-byte aligned) their head records
+static size_t rec_offset(uint64_t n) { return (size_t(emit_tiles(n) + 1) * 8 + 127) & ~size_t(127); }
+
+size_t ndx_wah_emit_scratch_bytes(uint64_t n) {
+  return rec_offset(n) + size_t(emit_tiles(n)) * sizeof(TileRec) + 256;
+}
 
 int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl, uint32_t* d_words,
                  uint32_t* d_vstart, uint32_t* d_values, void* d_scratch, void* stream) {
@@ -569,24 +1073,45 @@ int ndx_wah_emit(const uint64_t* d_pairs, uint64_t n, void* d_ctl, uint32_t* d_w
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e) return e;
-  // per-device launch shape, computed once per device (thread-safe)
-  static int grid_for[64], rc_for[64];
+  // per-device launch shapes, computed once per device (thread-safe)
+  static int grid_for[64], grid_rows_for[64], rc_for[64];
   static std::once_flag once[64];
   std::call_once(once[dev & 63], [dev] {
     int& rc = rc_for[dev & 63];
     if ((rc = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)))) return;
-    int sms = 0, occ = 0;
+    if ((rc = cudaFuncSetAttribute(k_emit_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kEmitRowsSmem))))
+      return;
+    int sms = 0, occ = 0, occ_rows = 0;
     if ((rc = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return;
     if ((rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, kEmitThreads, kEmitSmem))) return;
+    if ((rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_rows, k_emit_rows, kEmitThreads, kEmitRowsSmem)))
+      return;
     grid_for[dev & 63] = sms * (occ > 0 ? occ : 1);
+    grid_rows_for[dev & 63] = sms * (occ_rows > 0 ? occ_rows : 1);
   });
   if (rc_for[dev & 63]) return rc_for[dev & 63];
   const uint64_t tiles = emit_tiles(n);
   uint64_t* agg = static_cast<uint64_t*>(d_scratch);
-  if ((e = cudaMemsetAsync(agg, 0, tiles * 8, s))) return e;
-  int grid = int(umin<uint64_t>(tiles, uint64_t(grid_for[dev & 63])));
+  TileRec* recs = reinterpret_cast<TileRec*>(static_cast<char*>(d_scratch) + rec_offset(n));
   Ctl* ctl = static_cast<Ctl*>(d_ctl);
+  k_tile_prep<<<unsigned(umin<uint64_t>((tiles + 255) / 256, 1184)), 256, 0, s>>>(agg, recs, uint32_t(tiles));
+  k_tile_heads<<<unsigned(kMaxRowsValues / kHeadsThreads), kHeadsThreads, 0, s>>>(ctl, recs, uint32_t(tiles),
+                                                                                  d_values);
+  if ((e = cudaGetLastError())) return e;
   int bulk_ok = (reinterpret_cast<uintptr_t>(d_pairs) & 15) == 0;
+  // the sorted stream's form is known on the device only: both emit kernels
+  // are launched, the one that does not apply returns at once
+  {
+    const uint32_t* rows = reinterpret_cast<const uint32_t*>(d_pairs);
+    int grid = int(umin<uint64_t>(tiles, uint64_t(grid_rows_for[dev & 63])));
+    void* args[] = {(void*)&rows,     (void*)&n,    (void*)&ctl, (void*)&d_words,
+                    (void*)&d_vstart, (void*)&recs, (void*)&agg, (void*)&bulk_ok};
+    if ((e = cudaLaunchCooperativeKernel((const void*)k_emit_rows, dim3(grid), dim3(kEmitThreads), args,
+                                         kEmitRowsSmem, s)))
+      return e;
+  }
+  int grid = int(umin<uint64_t>(tiles, uint64_t(grid_for[dev & 63])));
   void* args[] = {(void*)&d_pairs, (void*)&n,        (void*)&ctl, (void*)&d_words,
                   (void*)&d_vstart, (void*)&d_values, (void*)&agg, (void*)&bulk_ok};
   return cudaLaunchCooperativeKernel((const void*)k_emit, dim3(grid), dim3(kEmitThreads), args,

@@ -11,6 +11,7 @@ enum SortMode : uint32_t { kModeNone = 0, kModeWide = 1, kModeBytes = 2, kModeAB
 
 constexpr int kWideMaxBits = 11;                 // single pass up to 2048 buckets
 constexpr int kWideBuckets = 1 << kWideMaxBits;
+constexpr int kMaxRowsValues = 1 << 16;          // compact mode: keys share their top 16 bits
 
 struct SortPlan {
   uint32_t mode;           // SortMode
@@ -41,11 +42,23 @@ struct Ctl {
   uint32_t grid_bar[2];  // cooperative sort launch: arrivals, generation
   uint32_t hist_byte[4][256];
   uint32_t hist_wide[kWideBuckets];
+  uint32_t rows_form;  // 1: the sort wrote row ids only (values from vs / pk below)
+  uint64_t vs_agg[kMaxRowsValues / 1024];  // k_vs: present keys per block of 1024 | ready bit
   uint32_t zero_end;
   // ---- written by the plan kernel ----
   uint32_t epoch;      // look-back status tag of this build (from the sort scratch counter)
   uint32_t row_hi;     // largest row id of the build (row_base + n - 1), written by the sort
   SortPlan plan;
+  // ---- the sorted stream's values in rows form (wide and compact modes) ----
+  // The wide pass and pass B write row ids only; the values are the present
+  // keys in order, pk[i] holding rows [vs[i], vs[i+1]) of the stream
+  // (vs[nvals] = n).  Written by k_vs after the last pass from vs16
+  // (compact mode: where each low-16-bit key starts, present or not --
+  // written, every entry, by the pass-B tile holding its start).
+  uint32_t nvals;
+  uint32_t vs[kMaxRowsValues + 1];
+  uint32_t pk[kMaxRowsValues];
+  uint32_t vs16[kMaxRowsValues];
 };
 
 }  // namespace ndx

@@ -17,6 +17,7 @@
 
 #include "../../../include/ndx.h"
 #include "common.cuh"
+#include "wah_internal.cuh"
 
 namespace ndx {
 
@@ -37,56 +38,54 @@ __device__ __forceinline__ uint64_t lower_key(const uint64_t* pairs, uint64_t n,
   return lo;
 }
 
-// One thread per value of the local index: first / last chunk (from the
-// sorted pairs), leading and trailing ones-fill of the body, and the body
-// range (the words after the local leading zero-fill).
-__global__ void k_shard_meta(const uint64_t* __restrict__ pairs, uint64_t n,
+// Metadata of entry d: first / last chunk of the value (from the sorted
+// stream: rows form -- the value's rows are [vs[d], vs[d+1]) -- or pairs),
+// leading and trailing ones-fill of the body, and the body range (the words
+// after the local leading zero-fill).
+__device__ __forceinline__ ndx_shard_meta meta_of(const Ctl* ctl, const uint64_t* stream, uint64_t n,
+                                                  const uint32_t* __restrict__ entries,
+                                                  const uint32_t* __restrict__ words, uint64_t d) {
+  const uint32_t v = entries[3 * d], off = entries[3 * d + 1], len = entries[3 * d + 2];
+  ndx_shard_meta m;
+  m.value = v;
+  if (ctl->rows_form) {
+    const uint32_t* rows = reinterpret_cast<const uint32_t*>(stream);
+    m.f = __ldg(rows + ctl->vs[d]) / kChunkBits;
+    m.l = __ldg(rows + ctl->vs[d + 1] - 1) / kChunkBits;
+  } else {
+    const uint64_t lo = lower_key(stream, n, v);
+    const uint64_t hi = v == 0xffffffffu ? n : lower_key(stream, n, v + 1);
+    m.f = uint32_t(__ldg(stream + lo) >> 32) / kChunkBits;
+    m.l = uint32_t(__ldg(stream + hi - 1) >> 32) / kChunkBits;
+  }
+  m.skip = is_zero_fill(words[off]) ? 1u : 0u;
+  m.body_off = off + m.skip;
+  m.body_len = len - m.skip;
+  const uint32_t first = words[m.body_off], last = words[m.body_off + m.body_len - 1];
+  m.a = is_ones_fill(first) ? fill_chunks(first) : 0u;
+  m.z = is_ones_fill(last) ? fill_chunks(last) : 0u;
+  return m;
+}
+
+// One thread per value of the local index.
+__global__ void k_shard_meta(const uint64_t* __restrict__ stream, uint64_t n, const Ctl* ctl,
                              const uint32_t* __restrict__ entries, uint64_t D,
                              const uint32_t* __restrict__ words, ndx_shard_meta* __restrict__ meta) {
   for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < D;
-       d += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t v = entries[3 * d], off = entries[3 * d + 1], len = entries[3 * d + 2];
-    const uint64_t lo = lower_key(pairs, n, v);
-    const uint64_t hi = v == 0xffffffffu ? n : lower_key(pairs, n, v + 1);
-    ndx_shard_meta m;
-    m.value = v;
-    m.f = uint32_t(__ldg(pairs + lo) >> 32) / kChunkBits;
-    m.l = uint32_t(__ldg(pairs + hi - 1) >> 32) / kChunkBits;
-    m.skip = is_zero_fill(words[off]) ? 1u : 0u;
-    m.body_off = off + m.skip;
-    m.body_len = len - m.skip;
-    const uint32_t first = words[m.body_off], last = words[m.body_off + m.body_len - 1];
-    m.a = is_ones_fill(first) ? fill_chunks(first) : 0u;
-    m.z = is_ones_fill(last) ? fill_chunks(last) : 0u;
-    meta[d] = m;
-  }
+       d += uint64_t(gridDim.x) * blockDim.x)
+    meta[d] = meta_of(ctl, stream, n, entries, words, d);
 }
 
 // The same with the value count on the device (ctl's ndx_wah_counts) and a
 // capacity: at most `cap` records are written (the plan flags a shard whose
 // count exceeds it).
-__global__ void k_shard_meta_dev(const uint64_t* __restrict__ pairs, uint64_t n,
-                                 const uint32_t* __restrict__ entries, const ndx_wah_counts* counts,
-                                 uint64_t cap, const uint32_t* __restrict__ words,
-                                 ndx_shard_meta* __restrict__ meta) {
-  const uint64_t D = umin<uint64_t>(counts->distinct, cap);
+__global__ void k_shard_meta_dev(const uint64_t* __restrict__ stream, uint64_t n,
+                                 const uint32_t* __restrict__ entries, const Ctl* ctl, uint64_t cap,
+                                 const uint32_t* __restrict__ words, ndx_shard_meta* __restrict__ meta) {
+  const uint64_t D = umin<uint64_t>(ctl->distinct, cap);
   for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < D;
-       d += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t v = entries[3 * d], off = entries[3 * d + 1], len = entries[3 * d + 2];
-    const uint64_t lo = lower_key(pairs, n, v);
-    const uint64_t hi = v == 0xffffffffu ? n : lower_key(pairs, n, v + 1);
-    ndx_shard_meta m;
-    m.value = v;
-    m.f = uint32_t(__ldg(pairs + lo) >> 32) / kChunkBits;
-    m.l = uint32_t(__ldg(pairs + hi - 1) >> 32) / kChunkBits;
-    m.skip = is_zero_fill(words[off]) ? 1u : 0u;
-    m.body_off = off + m.skip;
-    m.body_len = len - m.skip;
-    const uint32_t first = words[m.body_off], last = words[m.body_off + m.body_len - 1];
-    m.a = is_ones_fill(first) ? fill_chunks(first) : 0u;
-    m.z = is_ones_fill(last) ? fill_chunks(last) : 0u;
-    meta[d] = m;
-  }
+       d += uint64_t(gridDim.x) * blockDim.x)
+    meta[d] = meta_of(ctl, stream, n, entries, words, d);
 }
 
 // One warp per piece: the optional lead word, then src_len words copied from
@@ -113,14 +112,14 @@ using namespace ndx;
 
 extern "C" {
 
-int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const uint32_t* d_entries,
+int ndx_wah_shard_meta(const uint64_t* d_pairs, uint64_t n, const void* d_ctl, const uint32_t* d_entries,
                        uint64_t n_entries, const uint32_t* d_words, ndx_shard_meta* d_meta,
                        void* stream) {
   if (n_entries == 0) return 0;
-  if (!d_pairs || !d_entries || !d_words || !d_meta || n == 0) return NDX_E_INVALID;
+  if (!d_pairs || !d_ctl || !d_entries || !d_words || !d_meta || n == 0) return NDX_E_INVALID;
   const int grid = int(umin<uint64_t>((n_entries + 255) / 256, 4096));
-  k_shard_meta<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_pairs, n, d_entries,
-                                                                     n_entries, d_words, d_meta);
+  k_shard_meta<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_pairs, n, static_cast<const Ctl*>(d_ctl), d_entries, n_entries, d_words, d_meta);
   return cudaGetLastError();
 }
 
@@ -130,7 +129,7 @@ int ndx_wah_shard_meta_dev(const uint64_t* d_pairs, uint64_t n, const uint32_t* 
   if (!d_pairs || !d_entries || !d_ctl || !d_words || !d_meta || n == 0 || cap == 0) return NDX_E_INVALID;
   const int grid = int(umin<uint64_t>((cap + 255) / 256, 148 * 8));
   k_shard_meta_dev<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      d_pairs, n, d_entries, static_cast<const ndx_wah_counts*>(d_ctl), cap, d_words, d_meta);
+      d_pairs, n, d_entries, static_cast<const Ctl*>(d_ctl), cap, d_words, d_meta);
   return cudaGetLastError();
 }
 

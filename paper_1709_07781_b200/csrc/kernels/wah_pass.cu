@@ -109,6 +109,7 @@ struct PassMisc {
   uint32_t sgb[2][32];     // pass B: group starts inside the tile per parity
   uint32_t kbg[33];        // pass B: key base (top bits | lo) of the tile's groups
   uint32_t rbg[33];        // pass B: row base (row_base + seg << 24) of the tile's groups
+  uint32_t own_first;      // pass B: first low byte whose value starts the tile owns
 };
 
 // Shared memory of one CTA: [in: TILE u32][R: H | S][cnt NB][gbase NB][run NB][Misc]
@@ -158,6 +159,9 @@ struct PassCtx {
   uint32_t* gbase;
   uint32_t* run;           // wide/A: running global digit offsets of the chunk
   PassMisc* m;
+  // pass B: the tile holding the start of low byte lo = threadIdx.x in pass
+  // A's order (its bucket start there), and the same for lo - 1
+  uint32_t lo_tile, lo_tile_prev;
 };
 
 template <int KIND>
@@ -349,11 +353,13 @@ __device__ __forceinline__ void chunk_tile(const PassCtx& c, uint64_t tile, int6
       out[c.gbase[(e >> 16) & 0xffu] + jj] = (e & 0xff000000u) | (segofs + (e & 0xffffu));
     }
   } else {
+    // rows form: the row ids only (the values are the plan's bucket starts, k_vs)
+    uint32_t* out = reinterpret_cast<uint32_t*>(a.X);
     const uint32_t rbase = a.row_base + uint32_t(ts);
 #pragma unroll 4
     for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
-      const uint32_t e = S[jj], d = e >> LB;
-      a.X[c.gbase[d] + jj] = uint64_t(c.kbase + d) | (uint64_t(rbase + (e & ((1u << LB) - 1))) << 32);
+      const uint32_t e = S[jj];
+      out[c.gbase[e >> LB] + jj] = rbase + (e & ((1u << LB) - 1));
     }
   }
   __syncthreads();
@@ -479,7 +485,10 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   const uint32_t dme = threadIdx.x;
   const uint64_t first = tile > 0 ? ld_relaxed_u64(&a.status[uint64_t(tile - 1) * NB + dme]) : 0ull;
   add_local<KIND, BITS>(H, dme, c.gbase[dme]);
-  __syncthreads();
+  // the low bytes whose value starts this tile owns (contiguous: P_lo grows with lo)
+  const bool own = c.lo_tile == tile;
+  if (own && (dme == 0 || c.lo_tile_prev != tile)) m->own_first = dme;
+  const int nown = __syncthreads_count(own);
   rank_to_tile<KIND, BITS>(H, x, rk2);
   __syncthreads();  // H dead: S may overwrite it
 
@@ -532,24 +541,54 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   }
 
   // ---- look-back: this tile's global base for my digit
+  const uint32_t dlocal = c.gbase[dme];
+  uint32_t vbase;
   {
-    const uint32_t cd = c.cnt[dme], local = c.gbase[dme];
+    const uint32_t cd = c.cnt[dme], local = dlocal;
     uint64_t excl = 0;
     if (tile > 0) {
       excl = lookback_from(a.status, tile, NB, dme, c.epoch, first);
       st_relaxed_u64(&st[dme], st_word(c.epoch, kStPrefix, excl + cd));
     }
     c.gbase[dme] = c.bstart[dme] + uint32_t(excl) - local;
+    vbase = c.bstart[dme] + uint32_t(excl);
   }
   __syncthreads();
+  // ---- value starts of the rows form: for each low byte lo whose first
+  // group begins in this tile (at pass-A position P_lo), key (dme, lo)
+  // starts after this digit's elements of the tile that lie before P_lo
+  // (those of groups < lo * nseg; the digit's run is in group order)
+  if (nown) {
+    const uint32_t lo0 = m->own_first, cd = c.cnt[dme];
+    for (uint32_t lo = lo0; lo < lo0 + uint32_t(nown); ++lo) {
+      const uint32_t gl = lo * c.nseg;
+      uint32_t before;
+      if (k == 0) {
+        before = g0 < gl ? cd : 0u;
+      } else {
+        uint32_t lo_i = 0, hi_i = cd;
+        while (lo_i < hi_i) {
+          const uint32_t mid = (lo_i + hi_i) >> 1;
+          if (g0 + G16[dlocal + mid] < gl)
+            lo_i = mid + 1;
+          else
+            hi_i = mid;
+        }
+        before = lo_i;
+      }
+      a.ctl->vs16[(dme << 8) | lo] = vbase + before;
+    }
+  }
 
-  // ---- scatter: the (key, row) pair rebuilt from the packed word
+  // ---- scatter, rows form: the row id rebuilt from the packed word (the
+  // keys are the value starts above)
+  uint32_t* out = reinterpret_cast<uint32_t*>(a.X);
   if (k == 0) {
-    const uint32_t kb = m->kbg[0], rb = m->rbg[0];
+    const uint32_t rb = m->rbg[0];
 #pragma unroll 4
     for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
-      const uint32_t e = S32[jj], d = e >> 24;
-      a.X[c.gbase[d] + jj] = uint64_t(kb | (d << 8)) | (uint64_t(rb + (e & 0xffffffu)) << 32);
+      const uint32_t e = S32[jj];
+      out[c.gbase[e >> 24] + jj] = rb + (e & 0xffffffu);
     }
   } else {
     for (uint32_t jj = threadIdx.x; jj < tn; jj += SH::THREADS) {
@@ -563,7 +602,8 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
         kb = c.kbase | lo;
         rb = a.row_base + (seg << kSegBits);
       }
-      a.X[c.gbase[d] + jj] = uint64_t(kb | (d << 8)) | (uint64_t(rb + (e & 0xffffffu)) << 32);
+      (void)kb;
+      out[c.gbase[d] + jj] = rb + (e & 0xffffffu);
     }
   }
   if (threadIdx.x == 0) claim_next_b(c, ctr, par);
@@ -578,6 +618,13 @@ __device__ __forceinline__ void run_lookback_b(PassCtx& c) {
   using SH = PassShape<kPassB>;
   uint32_t* ctr = &c.a.ctl->tile_ctr[kCtrB];
   PassMisc* m = c.m;
+  {
+    // P_lo = pass A's bucket start of lo; the last tile also owns P_lo == n
+    const uint32_t* bs = c.a.ctl->plan.bucket_start_byte[0];
+    auto owner = [&](uint32_t lo) { return umin(uint32_t(bs[lo] / SH::TILE), c.tiles - 1); };
+    c.lo_tile = owner(threadIdx.x);
+    c.lo_tile_prev = threadIdx.x ? owner(threadIdx.x - 1) : 0xffffffffu;
+  }
   if (threadIdx.x == 0) {
     mbar_init(&m->bar, 1);
     fence_mbar_init();

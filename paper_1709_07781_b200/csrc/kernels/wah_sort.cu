@@ -299,6 +299,70 @@ __global__ __launch_bounds__(1024) void k_plan(PlanArgs a, int stage) {
   }
 }
 
+// Rows form of the sorted stream (wide and compact modes): the present keys
+// in order and the stream position where each one's rows begin -- the value
+// heads the emit stage needs, so the passes write 4-byte row ids instead of
+// 8-byte (key, row) pairs.  Every key's start is known already (wide: the
+// plan's bucket starts; compact: pass B's vs16); a key is present when the
+// next one starts later.  One thread per key, 64 CTAs: ballot ranks inside
+// the CTA, the CTA's base from its predecessors' published counts (all CTAs
+// are resident, each waits on lower ones only).
+constexpr int kVsThreads = 1024;
+constexpr int kVsBlocks = kMaxRowsValues / kVsThreads;
+__global__ __launch_bounds__(kVsThreads) void k_vs(Ctl* ctl, uint64_t n) {
+  const SortPlan& p = ctl->plan;
+  const uint32_t mode = p.mode;
+  if (mode != kModeWide && mode != kModeAB) return;  // bytes mode: pairs (rows_form stays 0)
+  const bool wide = mode == kModeWide;
+  const uint32_t nb = wide ? (1u << p.wide_bits) : uint32_t(kMaxRowsValues);
+  if (blockIdx.x * kVsThreads >= nb) return;
+  const uint32_t* start = wide ? p.bucket_start_wide : ctl->vs16;
+  const uint32_t k = blockIdx.x * kVsThreads + threadIdx.x;
+  const uint32_t pk = k < nb ? start[k] : 0u;
+  const uint32_t pn = k + 1 < nb ? start[k + 1] : uint32_t(n);
+  const bool present = k < nb && pn > pk;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(kFull, present);
+  __shared__ uint32_t s_w[32], s_base;
+  if (lane == 0) s_w[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = s_w[lane];
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, d);
+      if (lane >= uint32_t(d)) x += y;
+    }
+    s_w[lane] = x - v;
+    const uint32_t total = __shfl_sync(kFull, x, 31);
+    constexpr uint64_t kReady = 1ull << 63;  // vs_agg is cleared with the control block
+    if (lane == 0) st_relaxed_u64(&ctl->vs_agg[blockIdx.x], kReady | total);
+    uint32_t before = 0;
+    for (uint32_t b = lane; b < blockIdx.x; b += 32) {
+      uint64_t w;
+      while (!((w = ld_relaxed_u64(&ctl->vs_agg[b])) & kReady)) __nanosleep(20);
+      before += uint32_t(w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(kFull, before, o);
+    if (lane == 0) {
+      s_base = before;
+      if ((blockIdx.x + 1) * kVsThreads >= nb) {  // the last block: the totals
+        ctl->nvals = before + total;
+        ctl->vs[before + total] = uint32_t(n);
+        ctl->rows_form = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (present) {
+    const uint32_t j = s_base + s_w[warp] + __popc(bal & ((1u << lane) - 1u));
+    ctl->vs[j] = pk;
+    ctl->pk[j] = wide ? p.base + k : (p.base | k);
+  }
+}
+
 // Per-chunk digit offsets of the first pass (wide or A): chunk c's run of
 // digit d starts at bucket_start[d] + the count of d in chunks < c.  One CTA
 // per 32 digits: warp g sums its slice of the chunks for every digit (lane),
@@ -842,7 +906,11 @@ int ndx_wah_sort(const uint32_t* d_keys, uint64_t n, uint32_t row_base, void* d_
   a.X = d_pairs;
   a.Y = d_tmp_pairs;
   a.row_base = row_base;
-  return launch_sort(a, 0, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int rc = launch_sort(a, 0, s);
+  if (rc) return rc;
+  k_vs<<<kVsBlocks, kVsThreads, 0, s>>>(a.ctl, n);
+  return cudaGetLastError();
 }
 
 static size_t round256(size_t b) { return (b + 255) & ~size_t(255); }

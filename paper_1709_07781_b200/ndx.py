@@ -77,7 +77,7 @@ SIGNATURES = [
     ("ndx_chunks_rows", ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp]),
     ("ndx_wah_encode_scratch_bytes", _sz, [_u64]),
     ("ndx_wah_encode", ctypes.c_int, [_vp, _u64, ctypes.c_int, _vp, _vp, _vp, _vp]),
-    ("ndx_wah_shard_meta", ctypes.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
+    ("ndx_wah_shard_meta", ctypes.c_int, [_vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_wah_shard_meta_dev", ctypes.c_int, [_vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp]),
     ("ndx_merge_plan_scratch_bytes", _sz, [_u64]),
     ("ndx_merge_plan", ctypes.c_int, [_vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),

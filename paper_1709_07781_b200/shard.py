@@ -234,7 +234,8 @@ class ShardBuilder:
         self.b.launch(keys, n, row_base)
         W, D = self.b.counts()
         meta = t.empty(max(D, 1) * 8, dtype=t.int32, device=keys.device)
-        ndx.check(self.b.lib.ndx_wah_shard_meta(ndx._ptr(self.b.pairs), n, ndx._ptr(self.b.entries), D,
+        ndx.check(self.b.lib.ndx_wah_shard_meta(ndx._ptr(self.b.pairs), n, ndx._ptr(self.b.ctl),
+                                               ndx._ptr(self.b.entries), D,
                                                ndx._ptr(self.b.words), ndx._ptr(meta),
                                                t.cuda.current_stream().cuda_stream), "shard_meta")
         return W, D, meta
