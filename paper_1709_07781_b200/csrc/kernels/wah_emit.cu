@@ -828,7 +828,9 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
   uint16_t* ho = reinterpret_cast<uint16_t*>(stage + 2 * kEmitTile);
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ uint32_t s_wt[2][kEmitWarps];
-  __shared__ uint32_t s_rw[kEmitWarps], s_rd[kEmitWarps];
+  __shared__ uint32_t s_wx[2][kEmitWarps];  // exclusive prefix of s_wt over the warps
+  __shared__ uint32_t s_tot[2];             // the tile's (words << 16 | value heads)
+  __shared__ uint64_t s_acc[2];             // aggregates below the pending tile: heads << 32 | words
   __shared__ uint32_t s_tile[2];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -860,6 +862,7 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
   };
 
   if (threadIdx.x == 0) {
+    s_acc[0] = s_acc[1] = 0;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
@@ -944,7 +947,11 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
       if (has) {
         uint32_t tot = 0;
 #pragma unroll
-        for (int w = 0; w < kEmitWarps; ++w) tot += s_wt[b][w];
+        for (int w = 0; w < kEmitWarps; ++w) {
+          s_wx[b][w] = tot;
+          tot += s_wt[b][w];
+        }
+        s_tot[b] = tot;
         st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32));
       }
       const uint32_t nt = has ? atomicAdd(ctr, 1u) : ntiles;
@@ -977,25 +984,14 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
         sw += uint32_t(s);
         sd += uint32_t(s >> 32) & 0x7fffffffu;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sw += __shfl_xor_sync(kFull, sw, o);
-        sd += __shfl_xor_sync(kFull, sd, o);
-      }
-      if (lane == 0) {
-        s_rw[warp] = sw;
-        s_rd[warp] = sd;
-      }
+      sw = __reduce_add_sync(kFull, sw);
+      sd = __reduce_add_sync(kFull, sd);
+      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_acc[pb]),
+                               (static_cast<unsigned long long>(sd) << 32) | sw);
       __syncthreads();
-      uint64_t W0 = prev_w, D0 = prev_d;
-      uint32_t tw = 0, td = 0;
-#pragma unroll
-      for (int w = 0; w < kEmitWarps; ++w) {
-        W0 += s_rw[w];
-        D0 += s_rd[w];
-        tw += s_wt[pb][w] >> 16;
-        td += s_wt[pb][w] & 0xffffu;
-      }
+      const uint64_t acc = s_acc[pb];
+      const uint64_t W0 = prev_w + uint32_t(acc), D0 = prev_d + (acc >> 32);
+      const uint32_t tw = s_tot[pb] >> 16, td = s_tot[pb] & 0xffffu;
       prev_w = W0;
       prev_d = D0;
       prev_tile = int64_t(pt);
@@ -1011,11 +1007,10 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
       for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) vstart[D0 + j] = uint32_t(W0 + ho[j]);
     }
     __syncthreads();
+    if (threadIdx.x == 0) s_acc[b] = 0;  // last read the iteration before; next added to the iteration after
 
     if (has) {
-      uint32_t wbase = 0;
-#pragma unroll
-      for (int w = 0; w < kEmitWarps; ++w) wbase += w < warp ? s_wt[b][w] : 0u;
+      const uint32_t wbase = s_wx[b][warp];
       const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
       const uint32_t* Rs = R + kHaloL + li0;
       if (small_rows)
