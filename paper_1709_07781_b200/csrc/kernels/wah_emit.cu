@@ -48,6 +48,9 @@ constexpr int kEmitWarps = kEmitThreads / 32;
 #ifndef NDX_EMIT_K
 #define NDX_EMIT_K 14
 #endif
+#ifndef NDX_EMIT_AGGPRE
+#define NDX_EMIT_AGGPRE 2
+#endif
 static_assert(NDX_EMIT_K % 2 == 0 && NDX_EMIT_K < 31, "span length");
 constexpr int kEmitK = NDX_EMIT_K;                      // consecutive elements per thread
 constexpr int kEmitTile = kEmitThreads * kEmitK;        // 1024
@@ -886,7 +889,7 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
     const bool full = has && by_bulk(tile);
     const uint32_t* R = buf0 + b * kRowsBuf;  // R[kHaloL + li] = rows[tile * kEmitTile + li]
     const uint32_t ts = tile * kEmitTile, li0 = threadIdx.x * kEmitK;
-    constexpr int kAggPre = 4;
+    constexpr int kAggPre = NDX_EMIT_AGGPRE;  // aggregates read ahead per thread (about one per CTA in all)
     uint64_t pre[kAggPre];
     const uint64_t agg_lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
     const uint64_t agg_hi = pending < 0 ? agg_lo : uint64_t(pending);
