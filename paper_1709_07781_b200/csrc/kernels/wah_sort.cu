@@ -64,7 +64,16 @@ static_assert(Shape<8>::TILE == kLegacyByteTile && Shape<kWideMaxBits>::TILE == 
 
 // ------------------------------------------------------------------ S1 ----
 
-constexpr int kHistThreads = 512;
+constexpr int kHistThreads = 512;  // k_hist_hi
+#ifndef NDX_HIST_THREADS
+#define NDX_HIST_THREADS 256
+#endif
+#ifndef NDX_HIST_MINB
+#define NDX_HIST_MINB 4
+#endif
+// k_hist: one chunk per CTA, every CTA resident at once (kMaxChunks <= SMs x
+// NDX_HIST_MINB), so no SM runs a last round of chunks alone
+constexpr int kHistCtaThreads = NDX_HIST_THREADS;
 
 // Key range, low-11-bit histogram and byte-1 histogram in one read of the
 // keys, counted per chunk of the first pass (chunk_begin): each CTA takes
@@ -73,7 +82,7 @@ constexpr int kHistThreads = 512;
 // group of four warps counts into its own copy so a skewed column's hot bins
 // are not one shared-memory hot spot.
 constexpr int kHistCopies = 4;
-__global__ __launch_bounds__(kHistThreads, 1) void k_hist(const uint32_t* __restrict__ keys, uint64_t n,
+__global__ __launch_bounds__(kHistCtaThreads, NDX_HIST_MINB) void k_hist(const uint32_t* __restrict__ keys, uint64_t n,
                                                           Ctl* ctl, uint32_t* __restrict__ chunk_hist,
                                                           uint32_t nchunk) {
   __shared__ uint32_t hws[kHistCopies][kWideBuckets], h1s[kHistCopies][256];
@@ -821,7 +830,7 @@ static int legacy_cfg(const LegacyCfg** out) {
       return;
     if ((rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_byte, k_pass_bytes, Shape<8>::THREADS, sb)))
       return;
-    if ((rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_hist, k_hist, kHistThreads, 0))) return;
+    if ((rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_hist, k_hist, kHistCtaThreads, 0))) return;
     c.occ_wide = umax(c.occ_wide, 1);
     c.occ_byte = umax(c.occ_byte, 1);
     c.occ_hist = umax(c.occ_hist, 1);
@@ -843,7 +852,7 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, char* status_
   uint32_t* chunk_hist = reinterpret_cast<uint32_t*>(status_buf + kChunkHistOffset);
   // one wave: every CTA resident (a second partial wave would run alone)
   const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * c->occ_hist, nchunk)));
-  k_hist<<<grid, kHistThreads, 0, s>>>(keys, n, ctl, chunk_hist, nchunk);
+  k_hist<<<grid, kHistCtaThreads, 0, s>>>(keys, n, ctl, chunk_hist, nchunk);
   PlanArgs pa;
   pa.keys = keys;
   pa.n = n;
