@@ -11,7 +11,8 @@ import subprocess
 import sys
 
 STAGE = {"k_hist": "plan", "k_plan": "plan", "k_hist_hi": "plan", "k_chunk_scan": "plan", "k_pass": "sort",
-         "k_tma_pass": "sort", "k_pass_bytes": "sort", "k_set_row_hi": "sort", "k_emit": "emit", "k_table": "table"}
+         "k_tma_pass": "sort", "k_pass_bytes": "sort", "k_set_row_hi": "sort", "k_vs": "sort",
+         "k_tile_prep": "emit", "k_tile_heads": "emit", "k_emit": "emit", "k_emit_rows": "emit", "k_table": "table"}
 
 
 def kernels(rep):
