@@ -103,13 +103,14 @@ struct PassShape {
 };
 
 struct PassMisc {
+  uint32_t lo_start[256];  // pass B: pass A's bucket start of each low byte (16-byte aligned)
   uint64_t bar;            // mbarrier of the input bulk copy
   uint32_t tile[2];        // pass B: tile taken for iteration parity 0/1
   uint32_t tg[2][2];       // pass B: tile_group[t], tile_group[t+1] per parity
   uint32_t sgb[2][32];     // pass B: group starts inside the tile per parity
   uint32_t kbg[33];        // pass B: key base (top bits | lo) of the tile's groups
   uint32_t rbg[33];        // pass B: row base (row_base + seg << 24) of the tile's groups
-  uint32_t own_first;      // pass B: first low byte whose value starts the tile owns
+  uint32_t own[2];         // pass B: low bytes whose starts the tile holds, first | count << 16, per parity
 };
 
 // Shared memory of one CTA: [in: TILE u32][R: H | S][cnt NB][gbase NB][run NB][Misc]
@@ -159,9 +160,6 @@ struct PassCtx {
   uint32_t* gbase;
   uint32_t* run;           // wide/A: running global digit offsets of the chunk
   PassMisc* m;
-  // pass B: the tile holding the start of low byte lo = threadIdx.x in pass
-  // A's order (its bucket start there), and the same for lo - 1
-  uint32_t lo_tile, lo_tile_prev;
 };
 
 template <int KIND>
@@ -421,6 +419,21 @@ __device__ __forceinline__ void group_starts(const PassCtx& c, int par) {  // wa
   const uint32_t g0 = c.m->tg[par][0], k = c.m->tg[par][1] - g0;
   if (k <= 32 && lane < k) cp_async4(&c.m->sgb[par][lane], c.a.gb + g0 + 1 + lane);
 }
+// The low bytes lo whose start P_lo (in pass A's order) lies in the tile --
+// a contiguous range, P_lo grows with lo; the last tile also takes P_lo == n.
+__device__ __forceinline__ void own_range(const PassCtx& c, uint32_t tile, int par) {  // warp 0
+  using SH = PassShape<kPassB>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t a = tile * uint32_t(SH::TILE);
+  const uint32_t b = tile + 1 == c.tiles ? uint32_t(c.n) + 1u : a + uint32_t(SH::TILE);
+  const uint4* p = reinterpret_cast<const uint4*>(c.m->lo_start) + 2 * lane;
+  const uint4 u = p[0], v = p[1];
+  uint32_t ca = (u.x < a) + (u.y < a) + (u.z < a) + (u.w < a) + (v.x < a) + (v.y < a) + (v.z < a) + (v.w < a);
+  uint32_t cb = (u.x < b) + (u.y < b) + (u.z < b) + (u.w < b) + (v.x < b) + (v.y < b) + (v.z < b) + (v.w < b);
+  ca = __reduce_add_sync(kFull, ca);
+  cb = __reduce_add_sync(kFull, cb);
+  if (lane == 0) c.m->own[par] = ca | ((cb - ca) << 16);
+}
 
 // Takes the next tile at the end of this one (claim order == processing
 // order, so a tile's predecessors are ahead of it when it looks back),
@@ -463,6 +476,7 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
     if (lane == 0) cp_async_wait_all();
     __syncwarp();
     group_starts(c, par);
+    own_range(c, tile, par);
   }
   __syncthreads();  // inbuf consumed; R free (previous scatter done)
 
@@ -485,10 +499,7 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   const uint32_t dme = threadIdx.x;
   const uint64_t first = tile > 0 ? ld_relaxed_u64(&a.status[uint64_t(tile - 1) * NB + dme]) : 0ull;
   add_local<KIND, BITS>(H, dme, c.gbase[dme]);
-  // the low bytes whose value starts this tile owns (contiguous: P_lo grows with lo)
-  const bool own = c.lo_tile == tile;
-  if (own && (dme == 0 || c.lo_tile_prev != tile)) m->own_first = dme;
-  const int nown = __syncthreads_count(own);
+  __syncthreads();
   rank_to_tile<KIND, BITS>(H, x, rk2);
   __syncthreads();  // H dead: S may overwrite it
 
@@ -558,9 +569,10 @@ __device__ __forceinline__ void lookback_tile(const PassCtx& c, uint32_t* ctr, u
   // group begins in this tile (at pass-A position P_lo), key (dme, lo)
   // starts after this digit's elements of the tile that lie before P_lo
   // (those of groups < lo * nseg; the digit's run is in group order)
+  const uint32_t ownw = m->own[par], nown = ownw >> 16;
   if (nown) {
-    const uint32_t lo0 = m->own_first, cd = c.cnt[dme];
-    for (uint32_t lo = lo0; lo < lo0 + uint32_t(nown); ++lo) {
+    const uint32_t lo0 = ownw & 0xffffu, cd = c.cnt[dme];
+    for (uint32_t lo = lo0; lo < lo0 + nown; ++lo) {
       const uint32_t gl = lo * c.nseg;
       uint32_t before;
       if (k == 0) {
@@ -618,13 +630,8 @@ __device__ __forceinline__ void run_lookback_b(PassCtx& c) {
   using SH = PassShape<kPassB>;
   uint32_t* ctr = &c.a.ctl->tile_ctr[kCtrB];
   PassMisc* m = c.m;
-  {
-    // P_lo = pass A's bucket start of lo; the last tile also owns P_lo == n
-    const uint32_t* bs = c.a.ctl->plan.bucket_start_byte[0];
-    auto owner = [&](uint32_t lo) { return umin(uint32_t(bs[lo] / SH::TILE), c.tiles - 1); };
-    c.lo_tile = owner(threadIdx.x);
-    c.lo_tile_prev = threadIdx.x ? owner(threadIdx.x - 1) : 0xffffffffu;
-  }
+  static_assert(SH::THREADS == 256, "one low byte per thread");
+  m->lo_start[threadIdx.x] = c.a.ctl->plan.bucket_start_byte[0][threadIdx.x];
   if (threadIdx.x == 0) {
     mbar_init(&m->bar, 1);
     fence_mbar_init();
@@ -639,6 +646,7 @@ __device__ __forceinline__ void run_lookback_b(PassCtx& c) {
   __syncthreads();
   if (threadIdx.x < 32 && m->tile[0] < c.tiles) {
     group_starts(c, 0);
+    own_range(c, m->tile[0], 0);
     cp_async_wait_all();
   }
   __syncthreads();
@@ -718,7 +726,6 @@ template <int MAXB, int V>
 __global__ void k_pass(SortArgs a, int which);  // legacy wide pass (wah_sort.cu)
 __global__ void k_pass_bytes(SortArgs a);        // legacy byte passes, one cooperative launch (wah_sort.cu)
 
-__global__ void k_set_row_hi(SortArgs a) { a.ctl->row_hi = a.row_base + uint32_t(a.n - 1); }  // read by emit
 
 // ---------------------------------------------------------------- host ----
 
@@ -777,7 +784,6 @@ int launch_sort_dispatch(const SortArgs& a, int legacy, int byte_grid, int legac
   int rc = pass_cfg(&c);
   if (rc) return rc;
   const int bulk_keys = (reinterpret_cast<uintptr_t>(a.in_keys) & 15u) == 0;
-  k_set_row_hi<<<1, 1, 0, s>>>(a);
   if (legacy) {
     k_pass<kWideMaxBits, 0><<<legacy_wide_grid, 512, kLegacyWideSmem, s>>>(a, -1);
   } else {

@@ -318,7 +318,8 @@ __global__ __launch_bounds__(1024) void k_plan(PlanArgs a, int stage) {
 // are resident, each waits on lower ones only).
 constexpr int kVsThreads = 1024;
 constexpr int kVsBlocks = kMaxRowsValues / kVsThreads;
-__global__ __launch_bounds__(kVsThreads) void k_vs(Ctl* ctl, uint64_t n) {
+__global__ __launch_bounds__(kVsThreads) void k_vs(Ctl* ctl, uint64_t n, uint32_t row_base) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->row_hi = row_base + uint32_t(n - 1);  // read by the emit
   const SortPlan& p = ctl->plan;
   const uint32_t mode = p.mode;
   if (mode != kModeWide && mode != kModeAB) return;  // bytes mode: pairs (rows_form stays 0)
@@ -918,7 +919,7 @@ int ndx_wah_sort(const uint32_t* d_keys, uint64_t n, uint32_t row_base, void* d_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int rc = launch_sort(a, 0, s);
   if (rc) return rc;
-  k_vs<<<kVsBlocks, kVsThreads, 0, s>>>(a.ctl, n);
+  k_vs<<<kVsBlocks, kVsThreads, 0, s>>>(a.ctl, n, row_base);
   return cudaGetLastError();
 }
 
