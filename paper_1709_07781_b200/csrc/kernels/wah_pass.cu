@@ -6,7 +6,9 @@
 // the shape allows:
 //
 //   wide   key range < 2^11 (C1, C3): ONE pass on digit = key - min.
-//          keys (4 B) in, (key, row) pairs (8 B) out; rows synthesised.
+//          keys (4 B) in, row ids (4 B) out, synthesised: the rows form
+//          of the sorted stream (the values are the plan's bucket starts,
+//          k_vs in wah_sort.cu).
 //   A, B   key range < 2^16 with both low bytes varying (C4, C5): two
 //          passes whose intermediate is a packed u32 instead of a pair.
 //     A    digit = key & 0xff.  Out: hb << 24 | (i & 0xffffff), where hb is
@@ -18,13 +20,15 @@
 //          begin inside it (tile_group).
 //     B    digit = hb.  The element's low byte and row segment are its
 //          "group" (lo, seg) -- the pass-A run it came from -- found from
-//          tile_group and GB by position.  Out: (key, row) pairs.
-//   Bytes per element: wide 12; A + B 8 + 12 = 20 (the u64 ping-pong of
+//          tile_group and GB by position.  Out: row ids (rows form); the
+//          tile holding the start of low byte lo in pass A's order writes
+//          where each key (hb, lo) starts (vs16).
+//   Bytes per element: wide 8; A + B 8 + 8 = 16 (the u64 ping-pong of
 //   the legacy byte passes, wah_sort.cu, moves 12 + 16 = 28).
 //
 // The first pass (wide or A) reads the keys in their original order, so
 // its digit offsets per chunk of keys come from the plan stage (k_hist
-// counts every chunk, k_chunk_scan scans the counts): each CTA walks its
+// counts every chunk, k_plan_scan scans the counts): each CTA walks its
 // chunks' tiles in order with running digit offsets in shared memory -- no
 // look-back and no waiting on other CTAs -- and copies its next tile in by
 // TMA while it works on the current one.  Pass B reads pass A's output, so

@@ -7,7 +7,8 @@
 //   S1  k_hist    one streaming read of the keys: key range (min/max) and the
 //                 digit histograms (bytes 0,1 and the low 11 bits) in smem,
 //                 flushed with one global atomic per bin per CTA.
-//       k_plan    picks the pass structure without a host round trip:
+//       k_plan_scan picks the pass structure without a host round trip
+//                 (and scans the first pass's per-chunk digit offsets):
 //                   range < 2048            -> wide: ONE pass on key - min
 //                   bytes 2,3 constant and
 //                   bytes 0,1 both varying  -> compact: passes A, B with a
@@ -16,7 +17,8 @@
 //                                              bytes that vary
 //                 and turns the histograms into bucket start offsets.  Only
 //                 when bytes 2/3 vary does it launch (in its own tail, CUDA
-//                 dynamic parallelism) their histogram and a second plan.
+//                 dynamic parallelism) their histogram and k_plan_hi.
+//       k_vs      (after the passes) the rows form's value starts.
 //   S2  the sort stage (launch_sort_dispatch, wah_pass.cu) launches one
 //                 kernel per pass kind; each returns at once unless the plan
 //                 picked it, so the host never waits for the plan.  The wide
@@ -226,85 +228,160 @@ struct PlanArgs {
   int hist_hi_grid;
 };
 
-// stage 0: after k_hist; stage 1: after k_hist_hi (launched by stage 0 only
-// when bytes 2/3 vary).  Every build takes a fresh look-back tag from the
-// counter in the status buffer's header, so statuses of earlier builds never
-// read as ready.
-__global__ __launch_bounds__(1024) void k_plan(PlanArgs a, int stage) {
+// The plan once bytes 2/3 were counted (tail-launched by k_plan_scan only
+// when they vary; general keys, pairs form).
+__global__ __launch_bounds__(1024) void k_plan_hi(PlanArgs a) { plan_bytes(a.ctl, a.n, 4); }
+
+// S1's plan and the first pass's per-chunk digit offsets, one launch.  Every
+// CTA makes the (small) plan in shared memory from the key range and the
+// histograms -- the same plan in every CTA -- and CTA 0 publishes it, taking
+// the build's look-back tag from the counter in the status buffer's header
+// (statuses of earlier builds never read as ready).  Then, for the wide and
+// compact modes, each CTA takes 32 digits: chunk c's run of digit d starts at
+// bucket_start[d] + the count of d in chunks < c (warp g sums its slice of
+// the chunks for every digit, the slices are scanned, each warp writes its
+// chunks' offsets).
+__global__ __launch_bounds__(1024) void k_plan_scan(PlanArgs a, const uint32_t* __restrict__ chunk_hist,
+                                                    uint32_t* __restrict__ chunk_off, uint32_t nchunk) {
   Ctl* ctl = a.ctl;
   const uint64_t n = a.n;
   SortPlan& p = ctl->plan;
-  if (stage == 1) {
-    plan_bytes(ctl, n, 4);
-    return;
-  }
-  __shared__ uint32_t s_mode, s_wrap, s_hi;
-  __shared__ uint32_t rot[kWideBuckets];
-  const uint32_t mn = ~ctl->max_not, mx = ctl->max_seen;
-  // byte 0's histogram is the low-11-bit one folded
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    uint32_t c = 0;
-    for (int j = 0; j < kWideBuckets / 256; ++j) c += ctl->hist_wide[i + 256 * j];
-    ctl->hist_byte[0][i] = c;
-  }
-  __syncthreads();
-  // The tags are 24 bits: after 2^21 builds they come round again, and a
-  // status left by a build one cycle ago (at tiles no build since has
-  // reached) would read as ready.  So on the wrap every status ever written
-  // -- below the high-water mark kept in the header -- is cleared first.
-  uint64_t* hwm = reinterpret_cast<uint64_t*>(a.epoch_counter) + 1;
-  if (threadIdx.x == 0) {
-    *hwm = umax(*hwm, status_bytes(n));
-    const uint32_t old = *a.epoch_counter;
-    s_wrap = old >= kEpochMax;
-    const uint32_t ep = old >= kEpochMax ? kEpochStep : old + kEpochStep;
-    *a.epoch_counter = ep;
-    ctl->epoch = ep;
-    ctl->min_key = mn;
-    ctl->max_key = mx;
-    ctl->n_lo = uint32_t(n);
-    ctl->n_hi = uint32_t(n >> 32);
-    const uint32_t range = mx - mn;
-    p.need_hi = 0;
-    if (range < uint32_t(kWideBuckets)) {
-      p.mode = kModeWide;
-      p.base = mn;
-      p.wide_bits = range == 0 ? 0 : 32 - __clz(range);
-      p.npasses = 1;
-      p.complete = 1;
-      for (int k = 0; k < 4; ++k) p.byte_active[k] = 0;
-    } else {
-      p.mode = kModeBytes;
-      p.need_hi = (mn >> 16) != (mx >> 16);
-      p.complete = !p.need_hi;
-    }
-    s_mode = p.mode;
-    s_hi = p.need_hi;
-  }
-  __syncthreads();
-  if (s_wrap) {  // once per 2^21 builds: every status ever written, cleared
-    uint4* q = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.epoch_counter) + kStatusOffset);
-    const uint64_t nq = (*hwm - kStatusOffset) / sizeof(uint4);
-    for (uint64_t i = threadIdx.x; i < nq; i += blockDim.x) q[i] = make_uint4(0, 0, 0, 0);
-  }
-  if (s_mode == kModeWide) {
-    const uint32_t nb = 1u << p.wide_bits;
+  __shared__ uint32_t s_h[kWideBuckets], s_bs[kWideBuckets], s_h1[256], s_bs1[256];
+  __shared__ uint32_t s_wrap;
+  const uint32_t mn = ~ctl->max_not, mx = ctl->max_seen, range = mx - mn;
+  const bool wide = range < uint32_t(kWideBuckets);
+  const uint32_t wide_bits = range == 0 ? 0u : 32u - __clz(range);
+  const bool need_hi = !wide && (mn >> 16) != (mx >> 16);
+  bool b0 = false, b1 = false;
+  if (wide) {
+    const uint32_t nb = 1u << wide_bits;
     for (uint32_t d = threadIdx.x; d < uint32_t(kWideBuckets); d += blockDim.x)
-      rot[d] = d < nb ? ctl->hist_wide[(d + mn) & (kWideBuckets - 1)] : 0;
+      s_h[d] = d < nb ? ctl->hist_wide[(d + mn) & (kWideBuckets - 1)] : 0u;
     __syncthreads();
-    block_excl_scan(rot, p.bucket_start_wide, kWideBuckets);
-  } else if (!s_hi) {
-    plan_bytes(ctl, n, 2);
-    if (threadIdx.x == 0 && a.allow_compact && p.byte_active[0] && p.byte_active[1]) {
-      // compact two-pass mode (wah_pass.cu): bytes 2/3 constant, 0/1 vary
-      p.mode = kModeAB;
-      p.base = mn & 0xffff0000u;
-      p.nseg = uint32_t(n_segments(n));
-      a.tile_group[ceil_div(n, kBTile)] = 256u * p.nseg - 1u;  // group of the position past the end
+    block_excl_scan(s_h, s_bs, kWideBuckets);
+  } else {
+    // byte 0's histogram is the low-11-bit one folded; byte 1's from k_hist
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      uint32_t c = 0;
+      for (int j = 0; j < kWideBuckets / 256; ++j) c += ctl->hist_wide[i + 256 * j];
+      s_h[i] = c;
+      s_h1[i] = ctl->hist_byte[1][i];
     }
-  } else if (threadIdx.x == 0) {
-    k_hist_hi<<<a.hist_hi_grid, kHistThreads, 0, cudaStreamTailLaunch>>>(a.keys, n, ctl);
-    k_plan<<<1, 1024, 0, cudaStreamTailLaunch>>>(a, 1);
+    __syncthreads();
+    b0 = s_h[mn & 255u] != n;
+    b1 = s_h1[(mn >> 8) & 255u] != n;
+    if (!need_hi) {
+      if (b0) block_excl_scan(s_h, s_bs, 256);
+      if (b1) block_excl_scan(s_h1, s_bs1, 256);
+    }
+  }
+  const bool ab = !wide && !need_hi && a.allow_compact && b0 && b1;
+
+  if (blockIdx.x == 0) {
+    // The tags are 24 bits: after 2^21 builds they come round again, and a
+    // status left by a build one cycle ago (at tiles no build since has
+    // reached) would read as ready.  So on the wrap every status ever written
+    // -- below the high-water mark kept in the header -- is cleared first.
+    uint64_t* hwm = reinterpret_cast<uint64_t*>(a.epoch_counter) + 1;
+    if (threadIdx.x == 0) {
+      *hwm = umax(*hwm, status_bytes(n));
+      const uint32_t old = *a.epoch_counter;
+      s_wrap = old >= kEpochMax;
+      const uint32_t ep = old >= kEpochMax ? kEpochStep : old + kEpochStep;
+      *a.epoch_counter = ep;
+      ctl->epoch = ep;
+      ctl->min_key = mn;
+      ctl->max_key = mx;
+      ctl->n_lo = uint32_t(n);
+      ctl->n_hi = uint32_t(n >> 32);
+      p.need_hi = need_hi;
+      if (wide) {
+        p.mode = kModeWide;
+        p.base = mn;
+        p.wide_bits = wide_bits;
+        p.npasses = 1;
+        p.complete = 1;
+        for (int k = 0; k < 4; ++k) p.byte_active[k] = 0;
+      } else if (need_hi) {
+        p.mode = kModeBytes;
+        p.complete = 0;
+        k_hist_hi<<<a.hist_hi_grid, kHistThreads, 0, cudaStreamTailLaunch>>>(a.keys, n, ctl);
+        k_plan_hi<<<1, 1024, 0, cudaStreamTailLaunch>>>(a);
+      } else {  // plan_bytes over bytes 0/1, then the compact mode when both vary
+        p.byte_active[0] = b0;
+        p.byte_active[1] = b1;
+        p.byte_active[2] = p.byte_active[3] = 0;
+        p.byte_order[0] = 0;
+        p.byte_order[1] = b0 ? 1u : 0u;
+        p.byte_order[2] = p.byte_order[3] = 0;
+        p.npasses = uint32_t(b0) + uint32_t(b1);
+        p.mode = kModeBytes;
+        p.complete = 1;
+        if (ab) {
+          p.mode = kModeAB;
+          p.base = mn & 0xffff0000u;
+          p.nseg = uint32_t(n_segments(n));
+          a.tile_group[ceil_div(n, kBTile)] = 256u * p.nseg - 1u;  // group of the position past the end
+        }
+      }
+    }
+    if (wide) {
+      for (int d = threadIdx.x; d < kWideBuckets; d += blockDim.x) p.bucket_start_wide[d] = s_bs[d];
+    } else {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        ctl->hist_byte[0][i] = s_h[i];
+        if (!need_hi && b0) p.bucket_start_byte[0][i] = s_bs[i];
+        if (!need_hi && b1) p.bucket_start_byte[1][i] = s_bs1[i];
+      }
+    }
+    __syncthreads();
+    if (s_wrap) {  // once per 2^21 builds: every status ever written, cleared
+      uint4* q = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.epoch_counter) + kStatusOffset);
+      const uint64_t nq = (*hwm - kStatusOffset) / sizeof(uint4);
+      for (uint64_t i = threadIdx.x; i < nq; i += blockDim.x) q[i] = make_uint4(0, 0, 0, 0);
+    }
+  }
+
+  // ---- the first pass's per-chunk digit offsets
+  if (!wide && !ab) return;
+  const uint32_t nb = wide ? (1u << wide_bits) : 256u;
+  if (blockIdx.x * 32 >= nb) return;
+  __shared__ uint32_t part[32][33];
+  const uint32_t lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const uint32_t d = blockIdx.x * 32 + lane;
+  auto count = [&](uint32_t c) -> uint32_t {
+    const uint32_t* h = chunk_hist + uint64_t(c) * kChunkHistWords;
+    return __ldg(h + (wide ? ((d + mn) & (kWideBuckets - 1)) : kWideBuckets + d));
+  };
+  // at most kMaxChunks / 32 chunks per warp: every load of the slice in
+  // flight at once
+  constexpr int kPer = int(kMaxChunks / 32);
+  const uint32_t c0 = uint32_t(uint64_t(nchunk) * g / 32), c1 = uint32_t(uint64_t(nchunk) * (g + 1) / 32);
+  uint32_t cnt[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) cnt[k] = (d < nb && c0 + k < c1) ? count(c0 + k) : 0u;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) sum += cnt[k];
+  part[g][lane] = sum;
+  __syncthreads();
+  if (g == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t t = part[k][lane];
+      part[k][lane] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  if (d < nb) {
+    uint32_t run = s_bs[d] + part[g][lane];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (c0 + k < c1) {
+        chunk_off[uint64_t(c0 + k) * kWideBuckets + d] = run;
+        run += cnt[k];
+      }
   }
 }
 
@@ -373,65 +450,6 @@ __global__ __launch_bounds__(kVsThreads) void k_vs(Ctl* ctl, uint64_t n, uint32_
   }
 }
 
-// Per-chunk digit offsets of the first pass (wide or A): chunk c's run of
-// digit d starts at bucket_start[d] + the count of d in chunks < c.  One CTA
-// per 32 digits: warp g sums its slice of the chunks for every digit (lane),
-// the slices are scanned, then each warp writes its chunks' offsets.
-__global__ __launch_bounds__(1024) void k_chunk_scan(const Ctl* ctl, const uint32_t* __restrict__ chunk_hist,
-                                                     uint32_t* __restrict__ chunk_off, uint32_t nchunk) {
-  const SortPlan& p = ctl->plan;
-  const uint32_t mode = p.mode;
-  uint32_t nb;
-  const uint32_t* bstart;
-  if (mode == kModeWide) {
-    nb = 1u << p.wide_bits;
-    bstart = p.bucket_start_wide;
-  } else if (mode == kModeAB) {
-    nb = 256;
-    bstart = p.bucket_start_byte[0];
-  } else {
-    return;
-  }
-  if (blockIdx.x * 32 >= nb) return;
-  __shared__ uint32_t part[32][33];
-  const uint32_t lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const uint32_t d = blockIdx.x * 32 + lane;
-  const uint32_t mn = ctl->min_key;
-  auto count = [&](uint32_t c) -> uint32_t {
-    const uint32_t* h = chunk_hist + uint64_t(c) * kChunkHistWords;
-    return __ldg(h + (mode == kModeWide ? ((d + mn) & (kWideBuckets - 1)) : kWideBuckets + d));
-  };
-  // at most kMaxChunks / 32 chunks per warp: every load of the slice in
-  // flight at once
-  constexpr int kPer = int(kMaxChunks / 32);
-  const uint32_t c0 = uint32_t(uint64_t(nchunk) * g / 32), c1 = uint32_t(uint64_t(nchunk) * (g + 1) / 32);
-  uint32_t cnt[kPer];
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) cnt[k] = (d < nb && c0 + k < c1) ? count(c0 + k) : 0u;
-  uint32_t sum = 0;
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) sum += cnt[k];
-  part[g][lane] = sum;
-  __syncthreads();
-  if (g == 0) {
-    uint32_t run = 0;
-    for (int k = 0; k < 32; ++k) {
-      const uint32_t t = part[k][lane];
-      part[k][lane] = run;
-      run += t;
-    }
-  }
-  __syncthreads();
-  if (d < nb) {
-    uint32_t run = bstart[d] + part[g][lane];
-#pragma unroll
-    for (int k = 0; k < kPer; ++k)
-      if (c0 + k < c1) {
-        chunk_off[uint64_t(c0 + k) * kWideBuckets + d] = run;
-        run += cnt[k];
-      }
-  }
-}
 
 // ------------------------------------------------------------------ S2 ----
 
@@ -862,9 +880,8 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, char* status_
   pa.tile_group = reinterpret_cast<uint32_t*>(status_buf + kTgOffset);
   pa.allow_compact = allow_compact;
   pa.hist_hi_grid = c->sms * 2;
-  k_plan<<<1, 1024, 0, s>>>(pa, 0);
-  k_chunk_scan<<<kWideBuckets / 32, 1024, 0, s>>>(ctl, chunk_hist,
-                                                   reinterpret_cast<uint32_t*>(status_buf + kChunkOffOffset), nchunk);
+  k_plan_scan<<<kWideBuckets / 32, 1024, 0, s>>>(pa, chunk_hist,
+                                                  reinterpret_cast<uint32_t*>(status_buf + kChunkOffOffset), nchunk);
   return cudaGetLastError();
 }
 
