@@ -656,24 +656,40 @@ __device__ __forceinline__ void span_scan_r(const uint32_t* R, const Heads& H, c
   const uint32_t g0 = ts + li0;
   uint32_t pc = div31<SMALL>(prv);
   uint32_t hm = 0, vm = 0, gaps = 0, acc = 0;
+  if (FULL && vb == 0) {
+    // no value head in the span (nearly every span): runs split at chunks only
 #pragma unroll
-  for (int j = 0; j < kEmitK; ++j) {
-    const uint32_t row = r[j], c = div31<SMALL>(row);
-    const uint32_t bp = row - c * kChunkBits;
-    bool vh = (vb >> j) & 1u, h = vh | (c != pc);
-    if (!FULL) {
-      const uint32_t g = g0 + j;
-      const bool valid = g < n;
-      vh = valid & (vh | (g == 0));
-      h = valid & (h | (g == 0));
+    for (int j = 0; j < kEmitK; ++j) {
+      const uint32_t row = r[j], c = div31<SMALL>(row);
+      const uint32_t bp = row - c * kChunkBits;
+      const bool h = c != pc;
+      const uint32_t gap = h ? c - pc - 1 : 0u;
+      gaps += gap != 0;
+      s.pk[j] = SMALL ? (gap << 5) | bp : gap;
+      hm |= uint32_t(h) << j;
+      acc = (h ? 0u : acc) | (1u << bp);
+      pc = c;
     }
-    const uint32_t gap = h ? (vh ? c : c - pc - 1) : 0u;
-    gaps += gap != 0;
-    s.pk[j] = SMALL ? (gap << 5) | bp : gap;
-    hm |= uint32_t(h) << j;
-    vm |= uint32_t(vh) << j;
-    acc = (h ? 0u : acc) | (1u << bp);
-    pc = c;
+  } else {
+#pragma unroll
+    for (int j = 0; j < kEmitK; ++j) {
+      const uint32_t row = r[j], c = div31<SMALL>(row);
+      const uint32_t bp = row - c * kChunkBits;
+      bool vh = (vb >> j) & 1u, h = vh | (c != pc);
+      if (!FULL) {
+        const uint32_t g = g0 + j;
+        const bool valid = g < n;
+        vh = valid & (vh | (g == 0));
+        h = valid & (h | (g == 0));
+      }
+      const uint32_t gap = h ? (vh ? c : c - pc - 1) : 0u;
+      gaps += gap != 0;
+      s.pk[j] = SMALL ? (gap << 5) | bp : gap;
+      hm |= uint32_t(h) << j;
+      vm |= uint32_t(vh) << j;
+      acc = (h ? 0u : acc) | (1u << bp);
+      pc = c;
+    }
   }
   const bool hN = ((vb >> kEmitK) & 1u) | (div31<SMALL>(nxt) != pc);
   uint32_t tm;
