@@ -849,7 +849,8 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
   __shared__ uint32_t s_wt[2][kEmitWarps];
   __shared__ uint32_t s_wx[2][kEmitWarps];  // exclusive prefix of s_wt over the warps
   __shared__ uint32_t s_tot[2];             // the tile's (words << 16 | value heads)
-  __shared__ uint64_t s_acc[2];             // aggregates below the pending tile: heads << 32 | words
+  __shared__ uint32_t s_accw[2], s_accd[2];  // aggregates below the pending tile: words, heads
+  __shared__ uint32_t s_full[2];             // the tile arrives by bulk copy (thread 0 decides)
   __shared__ uint32_t s_tile[2];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -881,13 +882,14 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
   };
 
   if (threadIdx.x == 0) {
-    s_acc[0] = s_acc[1] = 0;
+    s_accw[0] = s_accw[1] = s_accd[0] = s_accd[1] = 0;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
     const uint32_t t = atomicAdd(ctr, 1u);
     s_tile[0] = t;
-    if (t < ntiles && by_bulk(t)) bulk_fill(t, 0);
+    s_full[0] = t < ntiles && by_bulk(t);
+    if (s_full[0]) bulk_fill(t, 0);
   }
   __syncthreads();
 
@@ -902,7 +904,7 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
     const uint32_t tile = s_tile[b];
     const bool has = tile < ntiles;
     if (!has && pending < 0) break;
-    const bool full = has && by_bulk(tile);
+    const bool full = s_full[b];
     const uint32_t* R = buf0 + b * kRowsBuf;  // R[kHaloL + li] = rows[tile * kEmitTile + li]
     const uint32_t ts = tile * kEmitTile, li0 = threadIdx.x * kEmitK;
     constexpr int kAggPre = NDX_EMIT_AGGPRE;  // aggregates read ahead per thread (about one per CTA in all)
@@ -974,8 +976,10 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
         st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32));
       }
       const uint32_t nt = has ? atomicAdd(ctr, 1u) : ntiles;
+      const bool nfull = nt < ntiles && by_bulk(nt);
       s_tile[b ^ 1] = nt;
-      if (nt < ntiles && by_bulk(nt)) bulk_fill(nt, b ^ 1);
+      s_full[b ^ 1] = nfull;
+      if (nfull) bulk_fill(nt, b ^ 1);
     }
 
     if (pending >= 0) {
@@ -1005,11 +1009,12 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
       }
       sw = __reduce_add_sync(kFull, sw);
       sd = __reduce_add_sync(kFull, sd);
-      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_acc[pb]),
-                               (static_cast<unsigned long long>(sd) << 32) | sw);
+      if (lane == 0) {
+        atomicAdd(&s_accw[pb], sw);
+        atomicAdd(&s_accd[pb], sd);
+      }
       __syncthreads();
-      const uint64_t acc = s_acc[pb];
-      const uint64_t W0 = prev_w + uint32_t(acc), D0 = prev_d + (acc >> 32);
+      const uint64_t W0 = prev_w + s_accw[pb], D0 = prev_d + s_accd[pb];
       const uint32_t tw = s_tot[pb] >> 16, td = s_tot[pb] & 0xffffu;
       prev_w = W0;
       prev_d = D0;
@@ -1026,7 +1031,7 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
       for (uint32_t j = threadIdx.x; j < td; j += kEmitThreads) vstart[D0 + j] = uint32_t(W0 + ho[j]);
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_acc[b] = 0;  // last read the iteration before; next added to the iteration after
+    if (threadIdx.x == 0) s_accw[b] = s_accd[b] = 0;  // last read the iteration before; next added to the iteration after
 
     if (has) {
       const uint32_t wbase = s_wx[b][warp];
