@@ -216,6 +216,59 @@ def test_row_base_shards(builder, port, k_chunks):
     assert np.array_equal(got.entries, ents) and np.array_equal(got.words, words)
 
 
+def _column_from_counts(keys, counts, rng, shuffle=True):
+    """A column whose sorted stream has key keys[i] over counts[i] positions
+    (value starts at the prefix sums), rows in random order unless not
+    shuffled (then each key's rows are one contiguous range)."""
+    v = np.repeat(np.asarray(keys, dtype=np.uint32), counts)
+    if shuffle:
+        rng.shuffle(v)
+    return v
+
+
+@pytest.mark.parametrize("mode", ["wide", "compact"])
+@pytest.mark.parametrize("case", ["starts_at_buffer_edges", "heads_per_tile_sweep", "stretch_meets_next_value",
+                                  "stretch_after_value_start"])
+def test_rows_form_edges(builder, port, mode, case):
+    """The rows form (wah_emit.cu k_emit_rows): value starts on and around the
+    emit tiles' buffer edges (tile 3584, halo 32 before and 4 after), tiles
+    holding about kRecHeads = 60 heads (the record's inline list against the
+    walk over vs), and all-ones stretches that end exactly where the next
+    value's rows continue the row sequence (the stretch is bounded by the
+    value's extent, not by the rows)."""
+    rng = np.random.default_rng(zlib.crc32((mode + case).encode()))
+    base = 11 if mode == "wide" else 0x00050000
+    T = 3584
+
+    def keys(m):  # wide: consecutive keys; compact: spread over both low bytes, top half constant
+        return base + (1 if mode == "wide" else max(1, 65535 // m)) * np.arange(m)
+
+    if case == "starts_at_buffer_edges":
+        starts = sorted({0, 1, 31, 32, 33} | {t * T + d for t in range(1, 6) for d in (-33, -32, -31, -1, 0, 1, 3, 4, 5)})
+        n = 6 * T + 50
+        counts = np.diff(starts + [n])
+        v = _column_from_counts(keys(len(counts)), counts, rng)
+    elif case == "heads_per_tile_sweep":
+        counts = []
+        for c in range(52, 70):  # 3620 / c heads per buffer: 69 .. 52
+            counts += [c] * (2 * T // c)
+        counts = np.array(counts)
+        v = _column_from_counts(keys(len(counts)), counts, rng)
+    elif case == "stretch_meets_next_value":
+        # key i holds rows [r_i, r_{i+1}): every value is an all-ones stretch
+        # and the next value's first row is this value's last + 1
+        counts = rng.integers(20, 200, 300)
+        v = _column_from_counts(keys(len(counts)), counts, rng, shuffle=False)
+    else:
+        # long stretches that start right after another value's start, inside
+        # one emit tile and across tiles
+        counts = np.array([1, 61, 62, 93, 1, 31, 4000, 2, 7300, 30, 31, 32, 62, 93, 124] * 8)
+        v = _column_from_counts(keys(len(counts)), counts, rng, shuffle=False)
+    if mode == "wide":
+        assert int(v.max()) - int(v.min()) < 2048 or case == "heads_per_tile_sweep"
+    assert same(builder.build(v), port.reference_index(v)), (mode, case)
+
+
 @pytest.mark.parametrize("n", [2047, 2048, 2049, 2048 * 3 + 31, 8191, 8192, 8193, 16383, 16384, 16385,
                                16384 * 3 + 1, 4096 * 37])
 @pytest.mark.parametrize("kind", ["uniform", "clustered", "zipf"])
