@@ -19,7 +19,7 @@ cat $O/stages_c3.txt $O/stages_c4.txt | tail -8
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv \
   python bench.py --steps 3 --warmup 3 --e2e-steps 2 --no-cpu-baseline --no-extra > $O/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
 for C in C4 C3; do
-ncu --set full --clock-control none --import-source on -k regex:"k_hist|k_plan|k_chunk_scan|k_tma_pass|k_pass_bytes|k_vs" -c 8 \
+ncu --set full --clock-control none --import-source on -k regex:"k_hist|k_plan|k_tma_pass|k_pass_bytes|k_vs" -c 7 \
   -o $O/full_sort_$C -f python tools/stage_times.py $C --reps 1 > $O/ncu_full_sort_$C.log 2>&1; echo "ncu sort $C rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"k_tile|k_emit|k_table" -c 5 \
   -o $O/full_emit_$C -f python tools/stage_times.py $C --reps 1 > $O/ncu_full_emit_$C.log 2>&1; echo "ncu emit $C rc=$?"
