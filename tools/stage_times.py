@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--ref", action="store_true", help="also the oracle's digest of the same values (slow)")
     ap.add_argument("--no-flush", action="store_true", help="builds back to back (as bench.py), no L2 flush")
+    ap.add_argument("--stages", type=int, default=4, help="run only the first K stages (experiments)")
     a = ap.parse_args()
     v = gen.config_values(a.config, a.n or None)
     n = v.size
@@ -34,7 +35,7 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     flush = torch.empty(256 << 20, dtype=torch.int32, device="cuda")
     times = []
-    calls = b.stage_calls(keys, n)
+    calls = b.stage_calls(keys, n)[:a.stages]
     for rep in range(a.reps + 3):
         if not a.no_flush:
             flush.zero_()
@@ -44,9 +45,9 @@ def main():
             ev[i + 1].record(s)
         torch.cuda.synchronize()
         if rep >= 3:
-            times.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
+            times.append([ev[i].elapsed_time(ev[i + 1]) for i in range(len(calls))] + [0.0] * (4 - len(calls)))
     t = np.median(np.array(times), axis=0)
-    W, D = b.counts()
+    W, D = b.counts() if a.stages == 4 else (0, 0)
     tot = t.sum()
     print(f"{a.config} n={n} W={W} D={D}")
     for name, x in zip(["plan", "sort", "emit", "table"], t):
