@@ -774,7 +774,13 @@ int first_pass_chunks(uint64_t n, uint32_t* k) {
   const PassCfg* c;
   int rc = pass_cfg(&c);
   if (rc) return rc;
-  *k = chunk_count(n, uint32_t(c->sms * c->occ_a));
+  // one chunk per resident pass-A CTA, or two when each still holds at
+  // least 16 blocks (2^18 keys): C4 -- 2^28 keys -- sorts 23 us faster in 888
+  // chunks than in 444; below that the per-chunk counts cost more than the
+  // smaller chunks gain (C3 +8 us in 888)
+  const uint64_t resident = uint64_t(c->sms) * c->occ_a;
+  const uint64_t blocks = ceil_div(n, kChunkBlock);
+  *k = chunk_count(n, uint32_t(blocks >= 2 * resident * 16 ? 2 * resident : resident));
   return 0;
 }
 

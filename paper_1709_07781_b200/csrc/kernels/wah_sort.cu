@@ -73,8 +73,8 @@ constexpr int kHistThreads = 512;  // k_hist_hi
 #ifndef NDX_HIST_MINB
 #define NDX_HIST_MINB 4
 #endif
-// k_hist: one chunk per CTA, every CTA resident at once (kMaxChunks <= SMs x
-// NDX_HIST_MINB), so no SM runs a last round of chunks alone
+// k_hist: every CTA resident at once, each with the same number of chunks,
+// so no SM runs a last round of chunks alone
 constexpr int kHistCtaThreads = NDX_HIST_THREADS;
 
 // Key range, low-11-bit histogram and byte-1 histogram in one read of the
@@ -870,7 +870,9 @@ static int launch_plan(const uint32_t* keys, uint64_t n, Ctl* ctl, char* status_
   if ((rc = first_pass_chunks(n, &nchunk))) return rc;
   uint32_t* chunk_hist = reinterpret_cast<uint32_t*>(status_buf + kChunkHistOffset);
   // one wave: every CTA resident (a second partial wave would run alone)
-  const int grid = int(umax<uint64_t>(1, umin<uint64_t>(uint64_t(c->sms) * c->occ_hist, nchunk)));
+  // the same number of chunks per CTA everywhere (every CTA resident)
+  const uint64_t per = ceil_div(nchunk, uint64_t(c->sms) * c->occ_hist);
+  const int grid = int(umax<uint64_t>(1, ceil_div(nchunk, per)));
   k_hist<<<grid, kHistCtaThreads, 0, s>>>(keys, n, ctl, chunk_hist, nchunk);
   PlanArgs pa;
   pa.keys = keys;
