@@ -778,9 +778,16 @@ int first_pass_chunks(uint64_t n, uint32_t* k) {
   // least 16 blocks (2^18 keys): C4 -- 2^28 keys -- sorts 23 us faster in 888
   // chunks than in 444; below that the per-chunk counts cost more than the
   // smaller chunks gain (C3 +8 us in 888)
+#ifndef NDX_CHUNK_WAVES
+#define NDX_CHUNK_WAVES 2
+#endif
+#ifndef NDX_CHUNK_MIN_BLOCKS
+#define NDX_CHUNK_MIN_BLOCKS 16
+#endif
   const uint64_t resident = uint64_t(c->sms) * c->occ_a;
   const uint64_t blocks = ceil_div(n, kChunkBlock);
-  *k = chunk_count(n, uint32_t(blocks >= 2 * resident * 16 ? 2 * resident : resident));
+  const uint64_t waves = blocks >= NDX_CHUNK_WAVES * resident * NDX_CHUNK_MIN_BLOCKS ? NDX_CHUNK_WAVES : 1;
+  *k = chunk_count(n, uint32_t(waves * resident));
   return 0;
 }
 

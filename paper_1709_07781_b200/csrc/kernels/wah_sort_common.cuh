@@ -152,7 +152,10 @@ static_assert((1 << kSegBits) % kATile == 0, "a pass-A tile never straddles a ro
 // scans the counts into per-chunk digit offsets, and the pass walks its
 // chunks in order with running offsets -- no look-back, no waiting.
 constexpr uint64_t kChunkBlock = 16384;
-constexpr uint32_t kMaxChunks = 1024;
+#ifndef NDX_MAX_CHUNKS
+#define NDX_MAX_CHUNKS 1024
+#endif
+constexpr uint32_t kMaxChunks = NDX_MAX_CHUNKS;
 static_assert(kChunkBlock % kWideTile == 0 && kChunkBlock % kATile == 0, "tiles nest in chunk blocks");
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // [first, last) element of chunk c of k over n keys
