@@ -20,6 +20,11 @@
 // are scanned inside the tile and across tiles, and the compacted words are
 // written to their final position -- no zero-padded fill/body arrays, no
 // host round trip.
+//
+// Two kernels, one per form of the sorted stream (wah_sort.cu): k_emit_rows
+// for the rows form (u32 row ids, the value heads from ctl->vs; the wide and
+// compact sorts) and k_emit for the pairs form (u64 (key, row); general
+// keys).  Both are launched; the one that does not apply returns at once.
 #include <cuda_runtime.h>
 
 #include <cstdint>
