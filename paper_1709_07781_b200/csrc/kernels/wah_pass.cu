@@ -214,7 +214,12 @@ __device__ __forceinline__ void rank_tile(uint16_t* H, uint32_t wofs, uint32_t t
   constexpr uint32_t NB = 1u << BITS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint16_t* Hw = H + warp * NB;
-  for (uint32_t d = lane; d < NB; d += 32) Hw[d] = 0;
+  if constexpr (KIND == kPassWide && NB >= 8) {  // 8 counters per 16-byte store
+    uint4* Hw4 = reinterpret_cast<uint4*>(Hw);
+    for (uint32_t i = lane; i < NB / 8; i += 32) Hw4[i] = make_uint4(0, 0, 0, 0);
+  } else {
+    for (uint32_t d = lane; d < NB; d += 32) Hw[d] = 0;
+  }
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < SH::IPT; ++r) {
@@ -260,6 +265,45 @@ __device__ __forceinline__ uint32_t warp_offsets(uint16_t* H, uint32_t d) {
     sum += cw;
   }
   return sum;
+}
+
+// 3a, eight digits at a time (digits 8g .. 8g+7, sixteen-bit lanes: a tile's
+//     counts stay below 2^16): warp offsets in place, the counts into cnt
+template <int KIND, int BITS>
+__device__ __forceinline__ void warp_offsets8(uint16_t* H, uint32_t g, uint32_t* cnt) {
+  constexpr uint32_t NG = (1u << BITS) / 8;
+  uint4* H4 = reinterpret_cast<uint4*>(H);
+  uint4 sum = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int w = 0; w < PassShape<KIND>::WARPS; ++w) {
+    const uint4 cw = H4[w * NG + g];
+    H4[w * NG + g] = sum;
+    sum.x = __vadd2(sum.x, cw.x);
+    sum.y = __vadd2(sum.y, cw.y);
+    sum.z = __vadd2(sum.z, cw.z);
+    sum.w = __vadd2(sum.w, cw.w);
+  }
+  uint4* c4 = reinterpret_cast<uint4*>(cnt + 8 * g);
+  c4[0] = make_uint4(sum.x & 0xffffu, sum.x >> 16, sum.y & 0xffffu, sum.y >> 16);
+  c4[1] = make_uint4(sum.z & 0xffffu, sum.z >> 16, sum.w & 0xffffu, sum.w >> 16);
+}
+// 3b, eight digits at a time: the tile-local starts lc[0..7] into every
+//     warp's offsets
+template <int KIND, int BITS>
+__device__ __forceinline__ void add_local8(uint16_t* H, uint32_t g, const uint32_t (&lc)[8]) {
+  constexpr uint32_t NG = (1u << BITS) / 8;
+  uint4* H4 = reinterpret_cast<uint4*>(H);
+  const uint4 p = make_uint4(lc[0] | (lc[1] << 16), lc[2] | (lc[3] << 16), lc[4] | (lc[5] << 16),
+                             lc[6] | (lc[7] << 16));
+#pragma unroll
+  for (int w = 0; w < PassShape<KIND>::WARPS; ++w) {
+    uint4 h = H4[w * NG + g];
+    h.x = __vadd2(h.x, p.x);
+    h.y = __vadd2(h.y, p.y);
+    h.z = __vadd2(h.z, p.z);
+    h.w = __vadd2(h.w, p.w);
+    H4[w * NG + g] = h;
+  }
 }
 
 // 3b. the tile-local digit start folded into every warp's offsets, then
@@ -312,16 +356,37 @@ __device__ __forceinline__ void chunk_tile(const PassCtx& c, uint64_t tile, int6
 
   rank_tile<KIND, BITS, FULL>(H, wofs, tn, x, rk2);
   __syncthreads();
-  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) c.cnt[d] = warp_offsets<KIND, BITS>(H, d);
-  __syncthreads();
-  block_excl_scan(c.cnt, c.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
-  for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
-    const uint32_t local = c.gbase[d], cd = c.cnt[d];
-    const uint32_t gstart = c.run[d];  // where this tile's run of d begins in the output
-    c.run[d] = gstart + cd;
-    c.gbase[d] = gstart - local;
-    add_local<KIND, BITS>(H, d, local);
-    if constexpr (KIND == kPassA) {
+  if constexpr (KIND == kPassWide) {
+    // up to 2^11 digits x 16 warps: eight digits per thread and 16-byte
+    // shared accesses (C3's pass 374 -> 356 us); pass A's 256 digits keep one
+    // thread per digit (eight per thread there measured 94 us slower on C4)
+    static_assert(NB >= 8, "eight digits per thread");
+    for (uint32_t g = threadIdx.x; g < NB / 8; g += SH::THREADS) warp_offsets8<KIND, BITS>(H, g, c.cnt);
+    __syncthreads();
+    block_excl_scan(c.cnt, c.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+    for (uint32_t g = threadIdx.x; g < NB / 8; g += SH::THREADS) {
+      uint32_t lc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t d = 8 * g + i;
+        const uint32_t local = c.gbase[d], cd = c.cnt[d];
+        const uint32_t gstart = c.run[d];  // where this tile's run of d begins in the output
+        lc[i] = local;
+        c.run[d] = gstart + cd;
+        c.gbase[d] = gstart - local;
+      }
+      add_local8<KIND, BITS>(H, g, lc);
+    }
+  } else {
+    for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) c.cnt[d] = warp_offsets<KIND, BITS>(H, d);
+    __syncthreads();
+    block_excl_scan(c.cnt, c.gbase, int(NB));  // gbase <- tile-local digit starts (syncs)
+    for (uint32_t d = threadIdx.x; d < NB; d += SH::THREADS) {
+      const uint32_t local = c.gbase[d], cd = c.cnt[d];
+      const uint32_t gstart = c.run[d];  // where this tile's run of d begins in the output
+      c.run[d] = gstart + cd;
+      c.gbase[d] = gstart - local;
+      add_local<KIND, BITS>(H, d, local);
       // segment starts, and the pass-B tiles that begin inside this run
       const uint32_t seg = uint32_t(ts >> kSegBits);
       if ((ts & ((1ull << kSegBits) - 1)) == 0) a.gb[d * c.nseg + seg] = gstart;
