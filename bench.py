@@ -424,7 +424,9 @@ def run_sharded(args, cfg, world, rank, local):
         "result_check": check,
         "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * n_r,
                 "d2h_bytes_per_step": 4 * slice_words + (12 * D if rank == 0 else 0), "ms_per_step": e2e_ms},
-        "gpu_launches": 13 * K,
+        # per step: the shard chain's 13 kernels (plan 2, sort 5, emit 4, table 1,
+        # meta 1), the merge plan's 7 (5 + two scans) and the pull (N > 1)
+        "gpu_launches": (13 + 7 + (1 if world > 1 else 0)) * K,
         "clocks": clk,
     }
     if rank == 0:
@@ -692,7 +694,10 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": e2e_steps,
                 "pipelined": "2 deep: step i+1 upload (H2D) and build overlap step i result copy (D2H on the copy engines)",
                 "result_check_ok": e2e_ok, "result_digest": e2e_digest, "sync_call_ms": e2e_sync_ms},
-        "gpu_launches": 11 * K,
+        # per build: plan 2 (k_hist, k_plan_scan), sort 5 (three TMA pass kinds,
+        # k_pass_bytes, k_vs), emit 4 (k_tile_prep, k_tile_heads, k_emit_rows,
+        # k_emit), table 1 -- the launches that return at once included
+        "gpu_launches": 12 * K,
         "clocks": clk,
     }
     if world == 1 and args.config == "C4" and not args.no_extra:
