@@ -309,6 +309,72 @@ __device__ __forceinline__ uint32_t warp_carry(const uint64_t* B, uint32_t ts, u
 
 constexpr uint64_t kAggReady = 1ull << 63;
 
+// Phase 1's scans across a warp's spans: the literal carried into each span
+// (a segmented OR-scan over the spans' trailing ORs, bit 31 = the span holds
+// a run head; the warp's first span gets wcarry) and, interleaved with it
+// (two independent shuffle chains), the sum of the spans' (words << 16 |
+// value heads).  Returns the inclusive sum; excl = the exclusive one.
+__device__ __forceinline__ uint32_t span_scans(const Span& sp, uint32_t wcarry, uint32_t& carry_in,
+                                               uint32_t& excl) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t x = (sp.hmask ? 0x80000000u : 0u) | sp.acc;
+  const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, d);
+    const uint32_t z = __shfl_up_sync(kFull, incl, d);
+    if (lane >= uint32_t(d)) {
+      if (!(x >> 31)) x |= y;
+      incl += z;
+    }
+  }
+  const uint32_t incl_lit = (x & kLiteralMask) | ((x >> 31) ? 0u : wcarry);
+  carry_in = __shfl_up_sync(kFull, incl_lit, 1);
+  if (lane == 0) carry_in = wcarry;
+  excl = incl - cnt;
+  return incl;
+}
+
+// The published (words, heads) aggregates of tiles [lo, hi): the first PRE
+// per thread are requested a phase early (agg_request), the rest and any
+// not yet published are read (waiting) when summed (agg_sum: this thread's
+// share, words and heads).
+template <int PRE>
+__device__ __forceinline__ void agg_request(const uint64_t* agg, uint64_t lo, uint64_t hi, uint64_t (&pre)[PRE]) {
+#pragma unroll
+  for (int j = 0; j < PRE; ++j) {
+    const uint64_t a = lo + threadIdx.x + uint64_t(j) * kEmitThreads;
+    pre[j] = a < hi ? ld_relaxed_u64(&agg[a]) : kAggReady;
+  }
+}
+template <int PRE>
+__device__ __forceinline__ void agg_sum(const uint64_t* agg, uint64_t lo, uint64_t hi, const uint64_t (&pre)[PRE],
+                                        uint32_t& sw, uint32_t& sd) {
+  sw = sd = 0;
+#pragma unroll
+  for (int j = 0; j < PRE; ++j) {
+    const uint64_t a = lo + threadIdx.x + uint64_t(j) * kEmitThreads;
+    if (a >= hi) break;
+    uint64_t s = pre[j];
+    while (!(s & kAggReady)) {
+      __nanosleep(32);
+      s = ld_relaxed_u64(&agg[a]);
+    }
+    sw += uint32_t(s);
+    sd += uint32_t(s >> 32) & 0x7fffffffu;
+  }
+  for (uint64_t j = lo + threadIdx.x + uint64_t(PRE) * kEmitThreads; j < hi; j += kEmitThreads) {
+    uint64_t s = ld_relaxed_u64(&agg[j]);
+    while (!(s & kAggReady)) {
+      __nanosleep(32);
+      s = ld_relaxed_u64(&agg[j]);
+    }
+    sw += uint32_t(s);
+    sd += uint32_t(s >> 32) & 0x7fffffffu;
+  }
+}
+
 template <bool SMALL>
 __device__ __forceinline__ void tile_phase1(bool full, const uint64_t* B,
                                             const uint64_t* __restrict__ pairs, uint32_t n,
@@ -388,11 +454,7 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
     uint64_t pre[kAggPre];
     const uint64_t agg_lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
     const uint64_t agg_hi = pending < 0 ? agg_lo : uint64_t(pending);
-#pragma unroll
-    for (int j = 0; j < kAggPre; ++j) {
-      const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
-      pre[j] = a < agg_hi ? ld_relaxed_u64(&agg[a]) : kAggReady;
-    }
+    agg_request(agg, agg_lo, agg_hi, pre);
     if (has) {
       if (full) {
         mbar_wait(&bar[b], (phase >> b) & 1u);
@@ -410,26 +472,7 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
         tile_phase1<false>(full, B, pairs, n32, ts, li0, sp);
         wcarry = warp_carry<false>(B, ts, uint32_t(warp) * 32 * kEmitK);
       }
-      // literal carried into each span: segmented OR-scan over the spans'
-      // trailing ORs (bit 31 = the span holds a run head)
-      // ... and, interleaved with it (two independent shuffle chains), the
-      // inclusive sum of the spans' (words << 16 | value heads)
-      uint32_t x = (sp.hmask ? 0x80000000u : 0u) | sp.acc;
-      const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, d);
-        const uint32_t z = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) {
-          if (!(x >> 31)) x |= y;
-          incl += z;
-        }
-      }
-      const uint32_t incl_lit = (x & kLiteralMask) | ((x >> 31) ? 0u : wcarry);
-      carry_in = __shfl_up_sync(kFull, incl_lit, 1);
-      if (lane == 0) carry_in = wcarry;
-      excl = incl - cnt;
+      const uint32_t incl = span_scans(sp, wcarry, carry_in, excl);
       if (lane == 31) s_wt[b][warp] = incl;
     }
     __syncthreads();
@@ -457,28 +500,8 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       // ---- write the previous tile out: global offsets first
       const int pb = b ^ 1;
       const uint64_t pt = uint64_t(pending);
-      uint32_t sw = 0, sd = 0;
-#pragma unroll
-      for (int j = 0; j < kAggPre; ++j) {
-        const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
-        if (a >= pt) break;
-        uint64_t s = pre[j];
-        while (!(s & kAggReady)) {
-          __nanosleep(32);
-          s = ld_relaxed_u64(&agg[a]);
-        }
-        sw += uint32_t(s);
-        sd += uint32_t(s >> 32) & 0x7fffffffu;
-      }
-      for (uint64_t j = agg_lo + threadIdx.x + uint64_t(kAggPre) * kEmitThreads; j < pt; j += kEmitThreads) {
-        uint64_t s = ld_relaxed_u64(&agg[j]);
-        while (!(s & kAggReady)) {
-          __nanosleep(32);
-          s = ld_relaxed_u64(&agg[j]);
-        }
-        sw += uint32_t(s);
-        sd += uint32_t(s >> 32) & 0x7fffffffu;
-      }
+      uint32_t sw, sd;
+      agg_sum(agg, agg_lo, pt, pre, sw, sd);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         sw += __shfl_xor_sync(kFull, sw, o);
@@ -916,11 +939,7 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
     uint64_t pre[kAggPre];
     const uint64_t agg_lo = prev_tile < 0 ? 0 : uint64_t(prev_tile);
     const uint64_t agg_hi = pending < 0 ? agg_lo : uint64_t(pending);
-#pragma unroll
-    for (int j = 0; j < kAggPre; ++j) {
-      const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
-      pre[j] = a < agg_hi ? ld_relaxed_u64(&agg[a]) : kAggReady;
-    }
+    agg_request(agg, agg_lo, agg_hi, pre);
     if (has) {
       if (full) {
         mbar_wait(&bar[b], (phase >> b) & 1u);
@@ -950,22 +969,7 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
           span_scan_r<false, false>(R, H, rows, vs, nvals, n32, ts, li0, sp);
         wcarry = warp_carry_r<false>(R, H, ts, uint32_t(warp) * 32 * kEmitK);
       }
-      uint32_t x = (sp.hmask ? 0x80000000u : 0u) | sp.acc;
-      const uint32_t cnt = (sp.nwords << 16) | uint32_t(__popc(sp.vmask));
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, d);
-        const uint32_t z = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) {
-          if (!(x >> 31)) x |= y;
-          incl += z;
-        }
-      }
-      const uint32_t incl_lit = (x & kLiteralMask) | ((x >> 31) ? 0u : wcarry);
-      carry_in = __shfl_up_sync(kFull, incl_lit, 1);
-      if (lane == 0) carry_in = wcarry;
-      excl = incl - cnt;
+      const uint32_t incl = span_scans(sp, wcarry, carry_in, excl);
       if (lane == 31) s_wt[b][warp] = incl;
     }
     __syncthreads();
@@ -990,28 +994,8 @@ __global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* _
     if (pending >= 0) {
       const int pb = b ^ 1;
       const uint64_t pt = uint64_t(pending);
-      uint32_t sw = 0, sd = 0;
-#pragma unroll
-      for (int j = 0; j < kAggPre; ++j) {
-        const uint64_t a = agg_lo + threadIdx.x + uint64_t(j) * kEmitThreads;
-        if (a >= pt) break;
-        uint64_t s = pre[j];
-        while (!(s & kAggReady)) {
-          __nanosleep(32);
-          s = ld_relaxed_u64(&agg[a]);
-        }
-        sw += uint32_t(s);
-        sd += uint32_t(s >> 32) & 0x7fffffffu;
-      }
-      for (uint64_t j = agg_lo + threadIdx.x + uint64_t(kAggPre) * kEmitThreads; j < pt; j += kEmitThreads) {
-        uint64_t s = ld_relaxed_u64(&agg[j]);
-        while (!(s & kAggReady)) {
-          __nanosleep(32);
-          s = ld_relaxed_u64(&agg[j]);
-        }
-        sw += uint32_t(s);
-        sd += uint32_t(s >> 32) & 0x7fffffffu;
-      }
+      uint32_t sw, sd;
+      agg_sum(agg, agg_lo, pt, pre, sw, sd);
       sw = __reduce_add_sync(kFull, sw);
       sd = __reduce_add_sync(kFull, sd);
       if (lane == 0) {
