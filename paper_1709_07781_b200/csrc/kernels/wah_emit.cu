@@ -397,7 +397,9 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
   uint32_t* stage = reinterpret_cast<uint32_t*>(buf0 + 2 * kEmitBuf);
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ uint32_t s_wt[2][kEmitWarps];
-  __shared__ uint32_t s_rw[kEmitWarps], s_rd[kEmitWarps];
+  __shared__ uint32_t s_wx[2][kEmitWarps];    // exclusive prefix of s_wt over the warps
+  __shared__ uint32_t s_tot[2];               // the tile's (words << 16 | value heads)
+  __shared__ uint32_t s_accw[2], s_accd[2];   // aggregates below the pending tile: words, heads
   __shared__ uint32_t s_tile[2];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -424,6 +426,7 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
   };
 
   if (threadIdx.x == 0) {
+    s_accw[0] = s_accw[1] = s_accd[0] = s_accd[1] = 0;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
@@ -480,7 +483,11 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       if (has) {
         uint32_t tot = 0;
 #pragma unroll
-        for (int w = 0; w < kEmitWarps; ++w) tot += s_wt[b][w];
+        for (int w = 0; w < kEmitWarps; ++w) {
+          s_wx[b][w] = tot;
+          tot += s_wt[b][w];
+        }
+        s_tot[b] = tot;
         st_relaxed_u64(&agg[tile], kAggReady | uint64_t(tot >> 16) | (uint64_t(tot & 0xffffu) << 32));
       }
       // take the next tile; its bulk copy overlaps the rest of this one
@@ -502,25 +509,15 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       const uint64_t pt = uint64_t(pending);
       uint32_t sw, sd;
       agg_sum(agg, agg_lo, pt, pre, sw, sd);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sw += __shfl_xor_sync(kFull, sw, o);
-        sd += __shfl_xor_sync(kFull, sd, o);
-      }
+      sw = __reduce_add_sync(kFull, sw);
+      sd = __reduce_add_sync(kFull, sd);
       if (lane == 0) {
-        s_rw[warp] = sw;
-        s_rd[warp] = sd;
+        atomicAdd(&s_accw[pb], sw);
+        atomicAdd(&s_accd[pb], sd);
       }
       __syncthreads();
-      uint64_t W0 = prev_w, D0 = prev_d;
-      uint32_t tw = 0, td = 0;
-#pragma unroll
-      for (int w = 0; w < kEmitWarps; ++w) {
-        W0 += s_rw[w];
-        D0 += s_rd[w];
-        tw += s_wt[pb][w] >> 16;
-        td += s_wt[pb][w] & 0xffffu;
-      }
+      const uint64_t W0 = prev_w + s_accw[pb], D0 = prev_d + s_accd[pb];
+      const uint32_t tw = s_tot[pb] >> 16, td = s_tot[pb] & 0xffffu;
       prev_w = W0;
       prev_d = D0;
       prev_tile = int64_t(pt);
@@ -542,12 +539,11 @@ __global__ __launch_bounds__(kEmitThreads, NDX_EMIT_MINB) void k_emit(const uint
       }
     }
     __syncthreads();  // the staging area is free again; s_tile[b^1] visible
+    if (threadIdx.x == 0) s_accw[b] = s_accd[b] = 0;  // last read the iteration before; next added to the iteration after
 
     if (has) {
       // ---- phase 2: this tile's words into the staging area
-      uint32_t wbase = 0;
-#pragma unroll
-      for (int w = 0; w < kEmitWarps; ++w) wbase += w < warp ? s_wt[b][w] : 0u;
+      const uint32_t wbase = s_wx[b][warp];
       const uint32_t o = (wbase >> 16) + (excl >> 16), h = (wbase & 0xffffu) + (excl & 0xffffu);
       if (small_rows)
         span_emit<true>(sp, B + li0, carry_in, o, h, stage, stage + 2 * kEmitTile,

@@ -25,7 +25,10 @@ def main():
     ap.add_argument("--no-flush", action="store_true", help="builds back to back (as bench.py), no L2 flush")
     ap.add_argument("--stages", type=int, default=4, help="run only the first K stages (experiments)")
     a = ap.parse_args()
-    v = gen.config_values(a.config, a.n or None)
+    if a.config == "U32":  # general keys (the pairs form): uniform over the whole u32 range
+        v = np.random.default_rng(7).integers(0, 1 << 32, a.n or (1 << 26), dtype=np.uint64).astype(np.uint32)
+    else:
+        v = gen.config_values(a.config, a.n or None)
     n = v.size
     b = ndx.WahBuilder(n)
     keys = torch.from_numpy(v.view(np.int32)).cuda()
