@@ -104,8 +104,10 @@ int ndx_memcpy_d2d_async(void* d_dst, const void* d_src, size_t bytes, void* str
  * decoupled look-back statuses, tagged per build so it never needs
  * clearing: its header keeps the tag counter and the high-water mark of the
  * statuses written, and the build whose 24-bit tags wrap (one in 2^21)
- * clears them all itself.  All sizes stay on the device: no stage needs a
- * host round trip.
+ * clears them all itself.  The emit's scratch (ndx_wah_emit_scratch_bytes(n)
+ * bytes, 128-byte aligned) holds its per-tile aggregates and value-head
+ * records and is cleared by the emit stage itself.  All sizes stay on the
+ * device: no stage needs a host round trip.
  * n must be below 2^31 (the index format's word offsets are u32).
  * ------------------------------------------------------------------------- */
 typedef struct {
