@@ -53,6 +53,9 @@ constexpr int kEmitWarps = kEmitThreads / 32;
 #ifndef NDX_EMIT_K
 #define NDX_EMIT_K 14
 #endif
+#ifndef NDX_EMIT_ROWS_MINB
+#define NDX_EMIT_ROWS_MINB 3
+#endif
 #ifndef NDX_EMIT_AGGPRE
 #define NDX_EMIT_AGGPRE 2
 #endif
@@ -858,7 +861,7 @@ __global__ __launch_bounds__(kHeadsThreads) void k_tile_heads(const Ctl* __restr
 
 // S3 over the rows form: k_emit's tile schedule, aggregates and write-out
 // (see there); three CTAs per SM fit beside the half-size buffers.
-__global__ __launch_bounds__(kEmitThreads, 3) void k_emit_rows(const uint32_t* __restrict__ rows, uint64_t n,
+__global__ __launch_bounds__(kEmitThreads, NDX_EMIT_ROWS_MINB) void k_emit_rows(const uint32_t* __restrict__ rows, uint64_t n,
                                                                Ctl* ctl, uint32_t* __restrict__ words,
                                                                uint32_t* __restrict__ vstart,
                                                                const TileRec* __restrict__ recs, uint64_t* agg,
